@@ -1,0 +1,340 @@
+#!/usr/bin/env python3
+"""Benchmark of the batched RSA hot path (arXiv 1407.1465) on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config NAME] [--impl ours|reference]
+
+Default workload (BASELINE.json metric "RSA-2048 modexps/sec (e=65537 and full
+d)"): one step = encrypt a 1M-packet batch with e = 65537, then decrypt the
+ciphertexts with the full private exponent d (configs[2] then configs[3]), all
+packets resident in HBM.  value = modexps per second (2 x packets per step),
+whole job.  Under torchrun each rank runs its own full-size batch (weak
+scaling, no collective in the timed region: packets are independent).
+
+Prints ONE JSON line on rank 0.  See DESIGN.md "Measurement" for every field.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import workload  # noqa: E402
+
+METRIC = "RSA-2048 modexps/sec (e=65537 and full d) at 1/2/4/8 B200; % of IMAD peak"
+R_PRODUCTS_PER_CLK_PER_SM = 32      # measured: profiles/r01_imad_peak.jsonl (IMAD.WIDE half rate)
+
+WORKLOADS = {
+    # name: (key, count, legs)   legs: list of (label, exponent field, input)
+    "rsa2048-roundtrip": ("rsa2048", 1 << 20, [("enc_e65537", "e"), ("dec_full_d", "d")]),
+    "rsa2048-enc": ("rsa2048", 1 << 20, [("enc_e65537", "e")]),
+    "rsa2048-dec": ("rsa2048", 1 << 20, [("dec_full_d", "d")]),
+    "u64-roundtrip": ("rsa64", 16 << 20, [("enc_e65537", "e"), ("dec_full_d", "d")]),
+    "toy-roundtrip": ("toy17947", 9, [("enc_e131", "e"), ("dec_d14171", "d")]),
+}
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="rsa2048-roundtrip", choices=sorted(WORKLOADS))
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=15.0, help="CPU-seconds budget of the oracle sample")
+    return ap.parse_args()
+
+
+# ------------------------------------------------------------------ clocks
+
+class ClockSampler:
+    FIELDS = ["clocks.sm", "clocks.max.sm", "clocks_event_reasons.sw_power_cap",
+              "clocks_event_reasons.hw_slowdown", "clocks_event_reasons.hw_thermal_slowdown",
+              "clocks_event_reasons.sw_thermal_slowdown", "power.draw"]
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.path = os.path.join("/tmp", f"rsa_bench_clocks_{os.getpid()}.csv")
+
+    def start(self):
+        try:
+            self.f = open(self.path, "w")
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), "--query-gpu=" + ",".join(self.FIELDS),
+                 "--format=csv,noheader,nounits", "-lms", "200"], stdout=self.f, stderr=subprocess.DEVNULL)
+        except (OSError, FileNotFoundError):
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        self.f.close()
+        sm, smax, reasons, power = [], [], set(), []
+        names = ["sw_power_cap", "hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown"]
+        with open(self.path) as f:
+            for line in f:
+                parts = [p.strip() for p in line.split(",")]
+                if len(parts) < len(self.FIELDS):
+                    continue
+                try:
+                    sm.append(float(parts[0]))
+                    smax.append(float(parts[1]))
+                    power.append(float(parts[6]))
+                except ValueError:
+                    continue
+                for nm, v in zip(names, parts[2:6]):
+                    if v.lower().startswith("active"):
+                        reasons.add(nm)
+        os.unlink(self.path)
+        loaded = [c for c in sm if smax and c > 0.5 * max(smax)] or sm
+        return {"sm_mhz": statistics.median(loaded) if loaded else None,
+                "sm_max_mhz": max(smax) if smax else None,
+                "reasons": sorted(reasons), "samples": len(sm),
+                "power_w_max": max(power) if power else None}
+
+
+# ------------------------------------------------------------------ oracle baseline
+
+def cpu_baseline(key: dict, base: np.ndarray, legs, cpu_seconds: float):
+    """The oracle (oracle/, plain C, as it stands) on the host cores, on a
+    bounded sample of the same workload: the first `k` packets, every leg."""
+    import oracle
+    cores = os.cpu_count() or 1
+    # calibrate one packet of the most expensive leg
+    t0 = time.perf_counter()
+    oracle.modexp_batch(base[:1], key[legs[-1][1]], key["n"], nthreads=1)
+    per = max(time.perf_counter() - t0, 1e-6) * len(legs)
+    k = int(max(cores, min(len(base), cpu_seconds / per)))
+    k = min(k, len(base))
+    t0 = time.perf_counter()
+    cur = base[:k]
+    for _, field in legs:
+        cur = oracle.modexp_batch(cur, key[field], key["n"], nthreads=cores)
+    wall = time.perf_counter() - t0
+    return {"value": k * len(legs) / wall, "unit": "modexp/s", "cores": cores, "kind": "oracle",
+            "sample": f"first {k} packets of the batch, {len(legs)} leg(s) each "
+                      f"({', '.join(l for l, _ in legs)}); {wall:.1f} s wall on {cores} threads"}
+
+
+def ncu_traffic(config: str):
+    """dram bytes per launch of the dominant kernel from the committed ncu
+    --set full summary (profiles/), or None."""
+    path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    try:
+        with open(path) as f:
+            return json.load(f).get(config)
+    except (OSError, ValueError):
+        return None
+
+
+# ------------------------------------------------------------------ arms
+
+def run_reference(args, rank, world):
+    """--impl reference: the oracle as it stands, on host cores, rank 0 only."""
+    if rank != 0:
+        return
+    key_name, count, legs = WORKLOADS[args.config]
+    key = workload.key(key_name)
+    nb = key["nbits"]
+    base = workload.packets(count, nb, n=key["n"], config_id=2)
+    import oracle
+    cores = os.cpu_count() or 1
+    t0 = time.perf_counter()
+    oracle.modexp_batch(base[:1], key[legs[-1][1]], key["n"], nthreads=1)
+    per = max(time.perf_counter() - t0, 1e-6) * len(legs)
+    budget = 120.0 / max(1, args.steps + args.warmup)          # whole run within a few minutes
+    k = int(min(count, max(cores, budget * cores / per)))
+    times = []
+    for it in range(args.warmup + args.steps):
+        t0 = time.perf_counter()
+        cur = base[:k]
+        for _, field in legs:
+            cur = oracle.modexp_batch(cur, key[field], key["n"], nthreads=cores)
+        if it >= args.warmup:
+            times.append(time.perf_counter() - t0)
+    ms = 1e3 * statistics.mean(times)
+    value = k * len(legs) / (ms / 1e3)
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "modexp/s", "n_gpus": 1,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "u32", "data": "synthetic",
+            "config": {"workload": args.config, "packets_per_step": k, "key": key_name,
+                       "note": "oracle (plain C bignum, Fig 5 L2R) on host cores; bounded sample per step"},
+            "cpu_baseline": {"value": value, "unit": "modexp/s", "cores": cores, "kind": "oracle",
+                             "sample": f"{k} packets x {len(legs)} legs per step"},
+            "e2e": {"value": value, "unit": "modexp/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def run_ours(args, rank, world, local_rank):
+    import torch
+    import torch.distributed as dist
+    import paper_1407_1465_b200 as R
+
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    key_name, count, legs = WORKLOADS[args.config]
+    key = workload.key(key_name)
+    nb, n = key["nbits"], key["n"]
+    s = workload.limbs_needed(nb)
+    # each rank: its own full-size batch (weak scaling); seeds differ per rank
+    base_np = workload.packets(count, nb, n=n, config_id=2 + 100 * rank)
+    base = torch.from_numpy(base_np.view(np.int32)).to(dev)
+    bufs = [base] + [torch.empty_like(base) for _ in legs]
+    stream = torch.cuda.current_stream(dev)
+    exps = [key[f] for _, f in legs]
+    plans = [R.rsa_plan_info(e, n, nb) for e in exps]
+
+    def step(evs=None):
+        for j, e in enumerate(exps):
+            if evs is not None:
+                evs[j][0].record(stream)
+            R.rsa_modexp_batch(bufs[j], e, n, nb, out=bufs[j + 1], stream=stream)
+            if evs is not None:
+                evs[j][1].record(stream)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    # correctness of the last warm-up round trip (GPU-side compare, cheap)
+    verified = bool(torch.equal(bufs[-1], bufs[0])) if len(legs) == 2 else None
+
+    clocks = ClockSampler(local_rank if "CUDA_VISIBLE_DEVICES" not in os.environ else 0)
+    if rank == 0:
+        clocks.start()
+        time.sleep(0.3)
+    leg_events = [[[torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)] for _ in legs]
+                  for _ in range(args.steps)]
+    t_start, t_end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    launches0 = R.rsa_kernel_launches()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    t_start.record(stream)
+    for k in range(args.steps):
+        step(leg_events[k])
+    t_end.record(stream)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    launches = R.rsa_kernel_launches() - launches0
+    clk = clocks.stop() if rank == 0 else None
+    elapsed_ms = t_start.elapsed_time(t_end)
+    leg_ms = [statistics.mean(leg_events[k][j][0].elapsed_time(leg_events[k][j][1]) for k in range(args.steps))
+              for j in range(len(legs))]
+    if world > 1:
+        t = torch.tensor([elapsed_ms] + leg_ms, device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        elapsed_ms, leg_ms = float(t[0]), [float(v) for v in t[1:]]
+
+    # ---- end to end through the public host API (pinned host buffers)
+    e2e = None
+    if not args.no_e2e and rank == 0:
+        host_in = torch.from_numpy(base_np.view(np.int32)).pin_memory()
+        host_mid = [torch.empty_like(host_in).pin_memory() for _ in legs]
+        R.rsa_modexp_batch_host(host_in, exps[0], n, nb, out=host_mid[0])      # warm
+        ts = []
+        for _ in range(max(1, min(args.steps, 3))):
+            t0 = time.perf_counter()
+            cur = host_in
+            for j, e in enumerate(exps):
+                R.rsa_modexp_batch_host(cur, e, n, nb, out=host_mid[j])
+                cur = host_mid[j]
+            ts.append(time.perf_counter() - t0)
+        e2e_s = statistics.median(ts)
+        nbytes = count * s * 4 * len(legs)
+        e2e = {"value": count * len(legs) / e2e_s, "unit": "modexp/s", "h2d_bytes_per_step": nbytes,
+               "d2h_bytes_per_step": nbytes, "ms_per_step": 1e3 * e2e_s,
+               "path": "rsa_modexp_batch_host per leg: pinned host -> device -> kernel -> host, chunk-pipelined"}
+        if len(legs) == 2:
+            e2e["verified"] = bool(torch.equal(host_mid[-1], host_in))
+
+    if rank != 0:
+        return
+    ms_per_step = elapsed_ms / args.steps
+    value = world * count * len(legs) / (ms_per_step / 1e3)
+    # ---- roofline of the dominant kernel
+    props = torch.cuda.get_device_properties(dev)
+    sms = props.multi_processor_count
+    peaks = {}
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            peaks = json.load(f)
+    except (OSError, ValueError):
+        pass
+    f_max = float(peaks.get("sm_max_mhz", 1965.0))
+    dom = max(range(len(legs)), key=lambda j: leg_ms[j])
+    S = plans[dom]["width_class"]
+    prod_per_mm = 2 * S * S + S
+    products = count * plans[dom]["montmuls"] * prod_per_mm
+    achieved = products / (leg_ms[dom] / 1e3) / 1e12
+    peak = R_PRODUCTS_PER_CLK_PER_SM * sms * f_max * 1e6 / 1e12
+    roofline = {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "Tprod/s", "frac": achieved / peak,
+                "traffic": ncu_traffic(args.config),
+                "kernel": f"modexp_kernel<{S}> ({legs[dom][0]})",
+                "algorithmic": f"{plans[dom]['montmuls']} montmul/packet x (2S^2+S = {prod_per_mm}) 32x32->64 "
+                               f"limb products x {count} packets per launch",
+                "peak_basis": f"{R_PRODUCTS_PER_CLK_PER_SM} products/clk/SM (IMAD.WIDE half rate, "
+                              f"profiles/r01_imad_peak.jsonl) x {sms} SMs x {f_max:.0f} MHz "
+                              f"(MEASURED_PEAKS sm_max_mhz)"}
+    if clk and clk.get("sm_mhz"):
+        roofline["frac_at_measured_clock"] = achieved / (R_PRODUCTS_PER_CLK_PER_SM * sms * clk["sm_mhz"] * 1e6 / 1e12)
+    legs_out = {}
+    for j, (label, field) in enumerate(legs):
+        legs_out[label] = {"ms": leg_ms[j], "modexp_per_s": world * count / (leg_ms[j] / 1e3),
+                           "montmuls_per_packet": plans[j]["montmuls"], "window": plans[j]["window"],
+                           "exp_bits": plans[j]["exp_bits"]}
+    cpu = None
+    if not args.no_cpu_baseline and world == 1:
+        cpu = cpu_baseline(key, base_np, legs, args.cpu_seconds)
+    line = {"metric": METRIC, "value": value, "unit": "modexp/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "u32", "data": "synthetic",
+            "config": {"workload": args.config, "packets_per_rank": count, "key": key_name + " (seeded, "
+                       "workload/keys.json)", "legs": [l for l, _ in legs], "modulus_bits": nb,
+                       "l2": f"inputs {count * s * 4 / 2**20:.0f} MiB per leg vs 126 MB L2"
+                             + (" (larger than L2)" if count * s * 4 > 126e6 else " (fits L2)"),
+                       "parallelism": f"dp{world} (independent shards, no collective in the timed region)"},
+            "legs": legs_out, "verified_roundtrip": verified, "roofline": roofline, "cpu_baseline": cpu,
+            "e2e": e2e, "gpu_launches": int(launches), "clocks": clk}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    args = parse()
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(local_rank)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    try:
+        run_ours(args, rank, world, local_rank)
+    finally:
+        if world > 1:
+            import torch.distributed as dist
+            dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

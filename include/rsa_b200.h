@@ -1,0 +1,143 @@
+/*
+ * rsa_b200.h -- C-ABI of the B200-native batched RSA library (librsa_b200.so).
+ *
+ * Method: arXiv 1407.1465, "Analysis of RSA Algorithm using GPU Programming"
+ * (PAPER.md = the paper's text).  The library implements the paper's
+ * data-parallel hot path -- C = M^e mod n for encryption and M = C^d mod n
+ * for decryption, applied independently to every packet (sec. 2;
+ * PAPER.md:65, sec. 3.3; sec. 11) -- for moduli from the
+ * paper's toy key (n = 17947) to 2048-bit keys, plus the key-generation check
+ * of Fig 1 and the packetisation of sec. 2.
+ *
+ * Conventions for every call:
+ *   - big integers are little-endian arrays of uint32_t limbs (limb 0 least
+ *     significant); a packet of an nbits-bit modulus has s = ceil(nbits/32)
+ *     limbs; a batch is packet-major: packet i occupies limbs [i*s, (i+1)*s);
+ *   - return value: RSA_OK (0) or a negative RSA_E* status; no call aborts,
+ *     prints or throws; rsa_strerror() names a status;
+ *   - no call keeps a pointer past its return except the asynchronous device
+ *     work of rsa_modexp_batch, which reads `base` and writes `out` in stream
+ *     order on `stream`.
+ */
+#ifndef RSA_B200_H
+#define RSA_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---- status codes ---------------------------------------------------- */
+#define RSA_OK            0
+#define RSA_EINVAL       -1   /* null pointer, bad size/length argument, partial overlap */
+#define RSA_ERANGE       -2   /* nbits out of [2, 2048], n >= 2^nbits, or e not in (1, phi) */
+#define RSA_EEVEN        -3   /* modulus even or < 3 (Montgomery needs gcd(n, 2) = 1) */
+#define RSA_ENOTPRIME    -4   /* p or q not prime (Fig 1: "random prime numbers") */
+#define RSA_EEQUAL       -5   /* p == q (Fig 1: "two different ... prime numbers") */
+#define RSA_ENOTCOPRIME  -6   /* gcd(e, phi) != 1 (Fig 1) */
+#define RSA_ECHAR        -7   /* encode: character outside a..z (after stripping spaces) */
+#define RSA_EODD         -8   /* encode: odd number of letters */
+#define RSA_ENOSPC       -9   /* output capacity too small */
+#define RSA_EPACKET     -10   /* decode: a digit pair > 25 */
+#define RSA_EBADKEY     -11   /* validate: d*e != 1 (mod phi) */
+#define RSA_ECUDA       -12   /* CUDA launch / allocation / copy failure */
+
+/* Largest modulus the GPU path accepts in this build (bits). */
+#define RSA_MAX_NBITS 2048
+
+const char* rsa_strerror(int status);
+
+/* ---- key generation check: Fig 1, PAPER.md:48-55 ---------------------
+ * Given p, q (pq_limbs limbs each, pq_limbs in [1, 64]) and e (e_limbs limbs,
+ * e_limbs in [1, 128]):  checks p and q prime (Miller-Rabin, deterministic
+ * below 2^64) and p != q; computes n = p*q and phi = (p-1)(q-1)
+ * (PAPER.md:53); checks 1 < e < phi and gcd(e, phi) = 1; computes
+ * d = e^-1 mod phi with 0 < d < phi ("d . e = 1 (mod phi(n))").
+ * Outputs are host buffers of 2*pq_limbs limbs each, caller-allocated.
+ * n_out and phi_out are written before the e checks (so ERANGE/ENOTCOPRIME
+ * still report them); d_out only on RSA_OK.  Synchronous, host only.
+ * Errors: RSA_EINVAL, RSA_ENOTPRIME, RSA_EEQUAL, RSA_ERANGE, RSA_ENOTCOPRIME. */
+int rsa_keygen_check(const uint32_t* p, const uint32_t* q, int pq_limbs,
+                     const uint32_t* e, int e_limbs,
+                     uint32_t* n_out, uint32_t* phi_out, uint32_t* d_out);
+
+/* ---- key validity: PAPER.md:33 ---------------------------------------
+ * residue_out (2*limbs limbs) = (d*e) mod phi, phi = (p-1)(q-1).  Returns
+ * RSA_OK when the residue is 1, RSA_EBADKEY otherwise (the paper's own sec. 2
+ * pair e=131, d=137, n=17947 gives residue 267).  All inputs
+ * have `limbs` limbs, limbs in [1, 64].  Synchronous, host only. */
+int rsa_validate_key(const uint32_t* e, const uint32_t* d, const uint32_t* p,
+                     const uint32_t* q, int limbs, uint32_t* residue_out);
+
+/* ---- batched modular exponentiation: the hot path ---------------------
+ * out[i] = base[i]^exp mod n for i < count  (C = M^e mod n, M = C^d mod n,
+ * PAPER.md:35; the same call serves encryption and decryption).
+ *   base, out : DEVICE pointers, [count][s] packet-major uint32 limbs,
+ *               s = ceil(nbits/32); caller-owned; out == base (exact
+ *               in-place) is allowed, any other overlap is RSA_EINVAL.
+ *               Any base[i] < 2^(32 s) is accepted (it is reduced mod n);
+ *               outputs are canonical, in [0, n).
+ *   exp, n    : HOST pointers of s limbs each; read before the call returns
+ *               (the caller may free them immediately).  exp = 0 gives 1.
+ *   nbits     : modulus width in bits, 2 <= nbits <= RSA_MAX_NBITS, and
+ *               n < 2^nbits; n must be odd and >= 3.
+ *   stream    : a cudaStream_t (NULL = legacy default stream).  The call is
+ *               asynchronous: it enqueues the kernel (and a stream-ordered
+ *               workspace allocation) and returns; completion is observed
+ *               through the stream.  count == 0 is a no-op returning RSA_OK.
+ * Errors: RSA_EINVAL, RSA_ERANGE, RSA_EEVEN, RSA_ECUDA. */
+int rsa_modexp_batch(const uint32_t* base, const uint32_t* exp, const uint32_t* n,
+                     int nbits, size_t count, uint32_t* out, void* stream);
+
+/* Same operation end to end from HOST memory: copies base_host to the device,
+ * exponentiates, and copies the result back to out_host, pipelining chunks
+ * so copies overlap compute (two streams).  base_host/out_host may be
+ * pageable or pinned (pinned is faster).  Synchronous: returns when out_host
+ * is written.  Errors: as rsa_modexp_batch. */
+int rsa_modexp_batch_host(const uint32_t* base_host, const uint32_t* exp, const uint32_t* n,
+                          int nbits, size_t count, uint32_t* out_host);
+
+/* Plan summary for (exp, n, nbits): the width class, window and the number
+ * of Montgomery multiplications each packet costs (for the roofline). */
+typedef struct {
+    int width_class;      /* S: limbs of the kernel's Montgomery arithmetic */
+    int s_io;             /* ceil(nbits/32): limbs per packet at this ABI */
+    int window;           /* sliding-window width (1 = binary, Fig 5) */
+    int table_entries;    /* per-packet window table entries */
+    int nops;             /* operations in the kernel's op list */
+    long long montmuls;   /* Montgomery multiplications per packet */
+    long long squarings;  /* of which squarings */
+    int exp_bits;         /* bit length of exp */
+    int grid;             /* persistent grid (CTAs) */
+    int block;            /* threads per CTA */
+} rsa_plan_info_t;
+
+int rsa_plan_info(const uint32_t* exp, const uint32_t* n, int nbits, rsa_plan_info_t* info);
+
+/* Force a sliding-window width for subsequent calls on this thread
+ * (0 = automatic, the default; 1..7 = fixed).  For tests and benchmarks. */
+int rsa_set_window(int w);
+
+/* ---- packet codec: sec. 2, PAPER.md:39-40 -----------------------------
+ * rsa_encode: strips ASCII spaces, maps a=00 .. z=25 and packs consecutive
+ * letter pairs as hi*100 + lo ("parallel encryption" ->
+ * 1500 1700 1111 0411 0413 0217 2415 1908 1413).  `packets` holds `cap`
+ * values; *count_out receives the packet count (or, on RSA_ECHAR, the index
+ * of the offending character in `text`; on RSA_ENOSPC, the count needed).
+ * rsa_decode: inverse (spaces are not recovered); `text` has `cap` bytes
+ * including the terminating NUL (needs 2*count + 1).
+ * Errors: RSA_EINVAL, RSA_ECHAR, RSA_EODD, RSA_ENOSPC, RSA_EPACKET. */
+int rsa_encode(const char* text, uint32_t* packets, size_t cap, size_t* count_out);
+int rsa_decode(const uint32_t* packets, size_t count, char* text, size_t cap);
+
+/* Number of kernels this library has launched since load (for the bench's
+ * gpu_launches accounting). */
+unsigned long long rsa_kernel_launches(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* RSA_B200_H */

@@ -1,0 +1,192 @@
+"""B200-native batched RSA modular exponentiation (arXiv 1407.1465 hot path).
+
+Thin Python binding over the C-ABI of ``librsa_b200.so`` (``include/rsa_b200.h``).
+Argument marshalling only: every step of the hot path runs in the library's
+CUDA kernels.  There is no CPU fallback -- importing this package without the
+built library raises ``ImportError``.
+
+Calls (same names as the C-ABI):
+  rsa_modexp_batch(base, exp, n, nbits, out=None, stream=None)   device tensors
+  rsa_modexp_batch_host(base, exp, n, nbits)                     host arrays (e2e)
+  rsa_keygen_check(p, q, e) -> (n, phi, d)                       Fig 1
+  rsa_validate_key(e, d, p, q) -> (ok, residue)
+  rsa_encode(text) / rsa_decode(packets)                         sec. 2 codec
+  rsa_plan_info(exp, n, nbits) -> dict
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "librsa_b200.so")
+
+RSA_OK, RSA_EINVAL, RSA_ERANGE, RSA_EEVEN = 0, -1, -2, -3
+RSA_ENOTPRIME, RSA_EEQUAL, RSA_ENOTCOPRIME = -4, -5, -6
+RSA_ECHAR, RSA_EODD, RSA_ENOSPC, RSA_EPACKET, RSA_EBADKEY, RSA_ECUDA = -7, -8, -9, -10, -11, -12
+RSA_MAX_NBITS = 2048
+
+EXPORTS = ["rsa_strerror", "rsa_keygen_check", "rsa_validate_key", "rsa_modexp_batch",
+           "rsa_modexp_batch_host", "rsa_plan_info", "rsa_set_window", "rsa_encode", "rsa_decode",
+           "rsa_kernel_launches"]
+
+if not os.path.exists(LIB_PATH):
+    raise ImportError(f"{LIB_PATH} is not built: run `python -m paper_1407_1465_b200.build` "
+                      "(no CPU fallback exists)")
+
+_lib = ctypes.CDLL(LIB_PATH)
+_u32p = ctypes.POINTER(ctypes.c_uint32)
+
+
+class RsaPlanInfo(ctypes.Structure):
+    _fields_ = [("width_class", ctypes.c_int), ("s_io", ctypes.c_int), ("window", ctypes.c_int),
+                ("table_entries", ctypes.c_int), ("nops", ctypes.c_int), ("montmuls", ctypes.c_longlong),
+                ("squarings", ctypes.c_longlong), ("exp_bits", ctypes.c_int), ("grid", ctypes.c_int),
+                ("block", ctypes.c_int)]
+
+
+_lib.rsa_strerror.restype = ctypes.c_char_p
+_lib.rsa_strerror.argtypes = [ctypes.c_int]
+_lib.rsa_keygen_check.argtypes = [_u32p, _u32p, ctypes.c_int, _u32p, ctypes.c_int, _u32p, _u32p, _u32p]
+_lib.rsa_validate_key.argtypes = [_u32p, _u32p, _u32p, _u32p, ctypes.c_int, _u32p]
+_lib.rsa_modexp_batch.argtypes = [ctypes.c_void_p, _u32p, _u32p, ctypes.c_int, ctypes.c_size_t,
+                                  ctypes.c_void_p, ctypes.c_void_p]
+_lib.rsa_modexp_batch_host.argtypes = [ctypes.c_void_p, _u32p, _u32p, ctypes.c_int, ctypes.c_size_t,
+                                       ctypes.c_void_p]
+_lib.rsa_plan_info.argtypes = [_u32p, _u32p, ctypes.c_int, ctypes.POINTER(RsaPlanInfo)]
+_lib.rsa_set_window.argtypes = [ctypes.c_int]
+_lib.rsa_encode.argtypes = [ctypes.c_char_p, _u32p, ctypes.c_size_t, ctypes.POINTER(ctypes.c_size_t)]
+_lib.rsa_decode.argtypes = [_u32p, ctypes.c_size_t, ctypes.c_char_p, ctypes.c_size_t]
+_lib.rsa_kernel_launches.restype = ctypes.c_ulonglong
+
+
+class RsaError(RuntimeError):
+    def __init__(self, code: int, where: str = ""):
+        msg = _lib.rsa_strerror(code).decode()
+        super().__init__(f"{where}: {msg} ({code})" if where else f"{msg} ({code})")
+        self.code = code
+
+
+def _check(rc: int, where: str):
+    if rc != RSA_OK:
+        raise RsaError(rc, where)
+
+
+def limbs(x: int, n: int) -> np.ndarray:
+    """Python int -> n little-endian uint32 limbs."""
+    if x < 0 or x >> (32 * n):
+        raise ValueError("value does not fit in %d limbs" % n)
+    return np.frombuffer(int(x).to_bytes(4 * n, "little"), dtype="<u4").astype(np.uint32)
+
+
+def to_int(a) -> int:
+    return int.from_bytes(np.ascontiguousarray(a, dtype="<u4").tobytes(), "little")
+
+
+def _p(a: np.ndarray):
+    return a.ctypes.data_as(_u32p)
+
+
+def nlimbs(nbits: int) -> int:
+    return (nbits + 31) // 32
+
+
+# ------------------------------------------------------------------ hot path
+
+def rsa_modexp_batch(base, exp: int, n: int, nbits: int, out=None, stream=None):
+    """out[i] = base[i]^exp mod n on the GPU (asynchronous on `stream`).
+
+    base: CUDA tensor [count, s] of int32/uint32 limbs (s = ceil(nbits/32)).
+    out:  CUDA tensor of the same shape (allocated if None; may be `base`).
+    stream: a torch.cuda.Stream, a raw cudaStream_t int, or None for the
+            current torch stream.
+    """
+    import torch
+    s = nlimbs(nbits)
+    if base.dim() != 2 or base.shape[1] != s or not base.is_cuda or base.element_size() != 4:
+        raise ValueError(f"base must be a CUDA [count, {s}] 32-bit tensor")
+    base = base.contiguous()
+    if out is None:
+        out = torch.empty_like(base)
+    if out.shape != base.shape or not out.is_contiguous() or out.element_size() != 4:
+        raise ValueError("out must be a contiguous tensor shaped like base")
+    if stream is None:
+        stream = torch.cuda.current_stream(base.device).cuda_stream
+    elif hasattr(stream, "cuda_stream"):
+        stream = stream.cuda_stream
+    E, N = limbs(exp, s), limbs(n, s)
+    with torch.cuda.device(base.device):
+        rc = _lib.rsa_modexp_batch(ctypes.c_void_p(base.data_ptr()), _p(E), _p(N), nbits, base.shape[0],
+                                   ctypes.c_void_p(out.data_ptr()), ctypes.c_void_p(stream))
+    _check(rc, "rsa_modexp_batch")
+    return out
+
+
+def rsa_modexp_batch_host(base: np.ndarray, exp: int, n: int, nbits: int, out: np.ndarray | None = None):
+    """End-to-end from host memory (H2D, kernel, D2H pipelined); synchronous."""
+    s = nlimbs(nbits)
+    base = np.ascontiguousarray(base, dtype=np.uint32) if isinstance(base, np.ndarray) else base
+    if out is None:
+        out = np.empty_like(base)
+    E, N = limbs(exp, s), limbs(n, s)
+    bp = base.ctypes.data if isinstance(base, np.ndarray) else base.data_ptr()
+    op = out.ctypes.data if isinstance(out, np.ndarray) else out.data_ptr()
+    rc = _lib.rsa_modexp_batch_host(ctypes.c_void_p(bp), _p(E), _p(N), nbits, base.shape[0], ctypes.c_void_p(op))
+    _check(rc, "rsa_modexp_batch_host")
+    return out
+
+
+def rsa_plan_info(exp: int, n: int, nbits: int) -> dict:
+    s = nlimbs(nbits)
+    info = RsaPlanInfo()
+    _check(_lib.rsa_plan_info(_p(limbs(exp, s)), _p(limbs(n, s)), nbits, ctypes.byref(info)), "rsa_plan_info")
+    return {f: getattr(info, f) for f, _ in RsaPlanInfo._fields_}
+
+
+def rsa_set_window(w: int) -> None:
+    _check(_lib.rsa_set_window(w), "rsa_set_window")
+
+
+def rsa_kernel_launches() -> int:
+    return int(_lib.rsa_kernel_launches())
+
+
+# ------------------------------------------------------------------ keys
+
+def rsa_keygen_check(p: int, q: int, e: int):
+    pl = max(nlimbs(max(p.bit_length(), q.bit_length(), 1)), 1)
+    el = nlimbs(max(e.bit_length(), 1))
+    n = np.zeros(2 * pl, np.uint32)
+    phi = np.zeros(2 * pl, np.uint32)
+    d = np.zeros(2 * pl, np.uint32)
+    rc = _lib.rsa_keygen_check(_p(limbs(p, pl)), _p(limbs(q, pl)), pl, _p(limbs(e, el)), el, _p(n), _p(phi), _p(d))
+    _check(rc, "rsa_keygen_check")
+    return to_int(n), to_int(phi), to_int(d)
+
+
+def rsa_validate_key(e: int, d: int, p: int, q: int):
+    L = max(nlimbs(max(v.bit_length(), 1)) for v in (e, d, p, q))
+    r = np.zeros(2 * L, np.uint32)
+    rc = _lib.rsa_validate_key(*(_p(limbs(v, L)) for v in (e, d, p, q)), L, _p(r))
+    if rc not in (RSA_OK, RSA_EBADKEY):
+        _check(rc, "rsa_validate_key")
+    return rc == RSA_OK, to_int(r)
+
+
+# ------------------------------------------------------------------ codec
+
+def rsa_encode(text: str):
+    cap = len(text) // 2 + 1
+    pk = np.zeros(cap, np.uint32)
+    cnt = ctypes.c_size_t(0)
+    _check(_lib.rsa_encode(text.encode("ascii"), _p(pk), cap, ctypes.byref(cnt)), "rsa_encode")
+    return [int(v) for v in pk[: cnt.value]]
+
+
+def rsa_decode(packets) -> str:
+    pk = np.ascontiguousarray(packets, dtype=np.uint32)
+    buf = ctypes.create_string_buffer(2 * len(pk) + 1)
+    _check(_lib.rsa_decode(_p(pk), len(pk), buf, len(buf)), "rsa_decode")
+    return buf.value.decode("ascii")

@@ -1,0 +1,41 @@
+"""Build librsa_b200.so in-tree with nvcc for sm_100a (no JIT, no torch ext)."""
+from __future__ import annotations
+
+import os
+import subprocess
+import sys
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+CSRC = os.path.join(HERE, "csrc")
+LIB = os.path.join(HERE, "librsa_b200.so")
+SOURCES = [os.path.join(CSRC, f) for f in ("modexp.cu", "rsa_abi.cpp")]
+DEPS = SOURCES + [os.path.join(CSRC, f) for f in ("mont.cuh", "plan.h", "host_bn.hpp")] + [
+    os.path.join(os.path.dirname(HERE), "include", "rsa_b200.h")]
+NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
+ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+
+
+def stale() -> bool:
+    if not os.path.exists(LIB):
+        return True
+    t = os.path.getmtime(LIB)
+    return any(os.path.getmtime(d) > t for d in DEPS)
+
+
+def build(force: bool = False, verbose: bool = False) -> str:
+    if not force and not stale():
+        return LIB
+    cmd = [NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-shared", "-Xcompiler", "-fPIC",
+           "-Xptxas", "-v" if verbose else "-O3", "-o", LIB + ".tmp", *SOURCES]
+    subprocess.check_call(cmd)
+    os.replace(LIB + ".tmp", LIB)
+    # the microbenchmark executable (roofline denominator), built alongside
+    mb = os.path.join(CSRC, "microbench", "imad_peak")
+    src = mb + ".cu"
+    if os.path.exists(src) and (force or not os.path.exists(mb) or os.path.getmtime(mb) < os.path.getmtime(src)):
+        subprocess.check_call([NVCC, *ARCH, "-O3", "-lineinfo", "-o", mb, src])
+    return LIB
+
+
+if __name__ == "__main__":
+    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv))

@@ -1,0 +1,65 @@
+// plan.h -- the launch plan shared by the host C-ABI (rsa_abi.cpp) and the
+// sm_100a kernels (modexp.cu).  Product code only; the oracle never sees it.
+//
+// A plan is the host-side key precompute of SURVEY.md sec. 8(a) step a1:
+//   n' = -n^-1 mod 2^32, R^2 mod n (R = 2^(32*S)), and the exponent recoded
+//   into a flat list of Montgomery-multiply operations (to-Montgomery, window
+//   table precompute, the left-to-right window scan, from-Montgomery).
+// The scan follows Fig 7 (sliding window) with reading Z6
+// (longest window ending in a 1-bit; A starts at the top window's entry);
+// w = 1 is exactly Fig 5 left-to-right binary.
+#pragma once
+#include <stdint.h>
+
+#define RSA_MAX_OPS 2048          // ops per plan (8 B each, kernel params)
+
+enum RsaOpKind : uint8_t {
+    RSA_OP_SQR = 0,    // A <- A * A * R^-1
+    RSA_OP_MUL = 1,    // A <- A * T[bidx] * R^-1   (T = per-thread window table)
+    RSA_OP_R2 = 2,     // A <- A * (R^2 mod n) * R^-1   (to Montgomery form)
+    RSA_OP_ONE = 3,    // A <- A * 1 * R^-1              (from Montgomery form)
+};
+
+enum RsaOpFlags : uint8_t {
+    RSA_F_LOADA = 1,   // before the op: A <- T[lidx]
+    RSA_F_STORE = 2,   // after the op:  T[sidx] <- A
+};
+
+struct __align__(8) RsaOp {
+    uint16_t rep;      // number of times the montmul is applied (>= 1)
+    uint8_t kind;      // RsaOpKind
+    uint8_t flags;     // RsaOpFlags
+    uint8_t bidx;      // table entry used as the b operand of RSA_OP_MUL
+    uint8_t lidx;      // table entry loaded into A (RSA_F_LOADA)
+    uint8_t sidx;      // table entry written from A (RSA_F_STORE)
+    uint8_t pad;
+};
+
+// Kernel parameters for width class S (32-bit limbs).  Passed by value as a
+// __grid_constant__ so n[] and r2[] are constant-bank operands of the IMADs.
+template <int S>
+struct ModexpParams {
+    const uint32_t* base;         // device, [count][s_io] LE limbs
+    uint32_t* out;                // device, [count][s_io]
+    void* table;                  // device workspace: ntab entries x S limbs x nthreads
+    unsigned long long count;
+    int s_io;                     // limbs per packet at the boundary (ceil(nbits/32))
+    int nops;
+    int ntab;                     // table entries (odd powers + g^2)
+    uint32_t n0inv;               // -n^-1 mod 2^32
+    uint32_t n[S];                // modulus, zero padded to S limbs
+    uint32_t r2[S];               // R^2 mod n, R = 2^(32 S)
+    RsaOp ops[RSA_MAX_OPS];
+};
+
+// host-visible summary of a plan (also exported through the C-ABI)
+struct RsaPlanInfo {
+    int width_class;              // S
+    int s_io;
+    int window;                   // sliding-window width w (1 = binary)
+    int table_entries;            // 2^(w-1) odd powers (+1 for g^2 when w > 1)
+    int nops;
+    long long montmuls;           // Montgomery multiplications per packet
+    long long squarings;          // of which squarings
+    int exp_bits;
+};

@@ -1,0 +1,499 @@
+// rsa_abi.cpp -- C-ABI of librsa_b200.so (declared in include/rsa_b200.h).
+//
+// Host side of the hot path: argument validation, the key precompute
+// (n', R^2 mod n, exponent recoding into an op
+// list), plan caching, stream-ordered workspace, kernel launch; plus the
+// Fig 1 key-generation check and the sec. 2 packet codec.  All arithmetic on
+// packets runs in the CUDA kernels of modexp.cu; nothing here falls back to
+// the CPU.
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <string.h>
+
+#include <atomic>
+#include <map>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../../include/rsa_b200.h"
+#include "host_bn.hpp"
+#include "plan.h"
+
+cudaError_t rsa_b200_launch(int S, const void* params, int sms, cudaStream_t stream);
+cudaError_t rsa_b200_grid(int S, int sms, int* grid, int* block, size_t* nthreads);
+size_t rsa_b200_params_size(int S);
+cudaError_t rsa_b200_fill_one(uint32_t* out, unsigned long long count, int s_io, int sms, cudaStream_t stream);
+
+using rsa_host::BN;
+
+namespace {
+
+std::atomic<unsigned long long> g_launches{0};
+thread_local int t_window_override = 0;
+
+// ------------------------------------------------------------------ plans
+
+struct Window {
+    int nsq;     // squarings before the multiply (ignored for the first window)
+    int val;     // odd window value, or -1 for trailing squarings only
+};
+
+// Fig 7 sliding-window recoding, reading Z6: from the top
+// bit, a zero bit costs one squaring; a one bit starts the longest window
+// e_i .. e_l of length <= w ending in a one; A <- A^(2^(i-l+1)) * g_val.
+static std::vector<Window> recode(const BN& e, int w) {
+    std::vector<Window> out;
+    int i = rsa_host::bits(e) - 1;
+    int pending = 0;
+    while (i >= 0) {
+        if (!rsa_host::bit(e, i)) {
+            pending++;
+            i--;
+            continue;
+        }
+        int l = i - w + 1;
+        if (l < 0) l = 0;
+        while (!rsa_host::bit(e, l)) l++;
+        int val = 0;
+        for (int j = i; j >= l; j--) val = (val << 1) | rsa_host::bit(e, j);
+        pending += i - l + 1;
+        out.push_back({pending, val});
+        pending = 0;
+        i = l - 1;
+    }
+    if (pending) out.push_back({pending, -1});
+    return out;
+}
+
+struct Plan {
+    int S = 0, s_io = 0, window = 1, ntab = 0, nops = 0, exp_bits = 0;
+    long long montmuls = 0, squarings = 0;
+    bool exp_zero = false;
+    std::vector<unsigned char> params;   // ModexpParams<S>, pointer fields patched per launch
+};
+
+static int width_class(int s_io) {
+    static const int classes[] = {2, 4, 8, 16, 32, 64};
+    for (int c : classes)
+        if (s_io <= c) return c;
+    return 0;
+}
+
+// Build the op list for window width w; returns false if it does not fit.
+static bool build_ops(const BN& e, int w, std::vector<RsaOp>* ops, int* ntab, long long* mm, long long* sq) {
+    std::vector<Window> win = recode(e, w);
+    const int nodd = 1 << (w - 1);
+    const int g2 = nodd;                      // table index of g^2 (w > 1)
+    *ntab = (w > 1) ? nodd + 1 : 1;
+    if (*ntab > 255) return false;
+    ops->clear();
+    *mm = 0;
+    *sq = 0;
+    auto push = [&](uint8_t kind, int rep, uint8_t flags, int bidx, int lidx, int sidx) {
+        RsaOp o;
+        memset(&o, 0, sizeof(o));
+        o.kind = kind;
+        o.rep = (uint16_t)rep;
+        o.flags = flags;
+        o.bidx = (uint8_t)bidx;
+        o.lidx = (uint8_t)lidx;
+        o.sidx = (uint8_t)sidx;
+        ops->push_back(o);
+        *mm += rep;
+        if (kind == RSA_OP_SQR) *sq += rep;
+    };
+    // to Montgomery form, g_1 = x R mod n -> T[0]
+    push(RSA_OP_R2, 1, RSA_F_STORE, 0, 0, 0);
+    if (w > 1) {
+        // g^2 -> T[g2];  g^(2j+1) = g^(2j-1) g^2 -> T[j]   (Fig 7 step 1)
+        push(RSA_OP_SQR, 1, RSA_F_STORE, 0, 0, g2);
+        for (int j = 1; j < nodd; j++)
+            push(RSA_OP_MUL, 1, RSA_F_STORE | (j == 1 ? RSA_F_LOADA : 0), g2, 0, j);
+    }
+    // exponent scan (Fig 7 step 3); A starts at the top window's entry
+    int first = win[0].val >> 1;
+    bool pending_load = true;
+    for (size_t k = 1; k < win.size(); k++) {
+        uint8_t fl = pending_load ? RSA_F_LOADA : 0;
+        // long runs of zero bits split into chunks of <= 65535 squarings
+        int nsq = win[k].nsq;
+        while (nsq > 0) {
+            int r = nsq > 65535 ? 65535 : nsq;
+            push(RSA_OP_SQR, r, fl, 0, first, 0);
+            fl = 0;
+            pending_load = false;
+            nsq -= r;
+        }
+        if (win[k].val >= 0) push(RSA_OP_MUL, 1, 0, win[k].val >> 1, 0, 0);
+    }
+    // from Montgomery form (+ the initial load if the scan had one window)
+    push(RSA_OP_ONE, 1, pending_load ? RSA_F_LOADA : 0, 0, first, 0);
+    return (int)ops->size() <= RSA_MAX_OPS;
+}
+
+template <int S>
+static void fill_params(Plan& pl, const BN& n, const std::vector<RsaOp>& ops) {
+    pl.params.assign(sizeof(ModexpParams<S>), 0);
+    ModexpParams<S>* p = reinterpret_cast<ModexpParams<S>*>(pl.params.data());
+    p->s_io = pl.s_io;
+    p->nops = (int)ops.size();
+    p->ntab = pl.ntab;
+    p->n0inv = rsa_host::neg_inv32(n[0]);
+    rsa_host::to_limbs(n, p->n, S);
+    BN r2 = rsa_host::pow2_mod(64 * S, n);      // R^2 mod n, R = 2^(32 S)
+    rsa_host::to_limbs(r2, p->r2, S);
+    for (size_t i = 0; i < ops.size(); i++) p->ops[i] = ops[i];
+}
+
+template <int S>
+static void patch_params(void* raw, const uint32_t* base, uint32_t* out, void* table, size_t count) {
+    ModexpParams<S>* p = reinterpret_cast<ModexpParams<S>*>(raw);
+    p->base = base;
+    p->out = out;
+    p->table = table;
+    p->count = count;
+}
+
+static void patch(int S, void* raw, const uint32_t* base, uint32_t* out, void* table, size_t count) {
+    switch (S) {
+    case 2: patch_params<2>(raw, base, out, table, count); break;
+    case 4: patch_params<4>(raw, base, out, table, count); break;
+    case 8: patch_params<8>(raw, base, out, table, count); break;
+    case 16: patch_params<16>(raw, base, out, table, count); break;
+    case 32: patch_params<32>(raw, base, out, table, count); break;
+    case 64: patch_params<64>(raw, base, out, table, count); break;
+    }
+}
+
+static std::mutex g_plan_mu;
+static std::map<std::string, Plan> g_plans;
+
+static int get_plan(const uint32_t* exp, const uint32_t* n, int nbits, Plan* out) {
+    const int s_io = (nbits + 31) / 32;
+    const int wov = t_window_override;
+    std::string key((const char*)&nbits, sizeof(int));
+    key.append((const char*)&wov, sizeof(int));
+    key.append((const char*)n, sizeof(uint32_t) * s_io);
+    key.append((const char*)exp, sizeof(uint32_t) * s_io);
+    {
+        std::lock_guard<std::mutex> lk(g_plan_mu);
+        auto it = g_plans.find(key);
+        if (it != g_plans.end()) {
+            *out = it->second;
+            return RSA_OK;
+        }
+    }
+    Plan pl;
+    pl.s_io = s_io;
+    pl.S = width_class(s_io);
+    if (!pl.S) return RSA_ERANGE;
+    BN N = rsa_host::from_limbs(n, s_io);
+    BN E = rsa_host::from_limbs(exp, s_io);
+    pl.exp_bits = rsa_host::bits(E);
+    if (E.empty()) {
+        pl.exp_zero = true;
+    } else {
+        std::vector<RsaOp> best_ops;
+        long long best = -1;
+        for (int w = 1; w <= 7; w++) {
+            if (wov && w != wov) continue;
+            std::vector<RsaOp> ops;
+            int ntab;
+            long long mm, sq;
+            if (!build_ops(E, w, &ops, &ntab, &mm, &sq)) continue;
+            if (best < 0 || mm < best) {
+                best = mm;
+                best_ops = ops;
+                pl.window = w;
+                pl.ntab = ntab;
+                pl.montmuls = mm;
+                pl.squarings = sq;
+            }
+        }
+        if (best < 0) return RSA_EINVAL;   // forced window does not fit
+        pl.nops = (int)best_ops.size();
+        switch (pl.S) {
+        case 2: fill_params<2>(pl, N, best_ops); break;
+        case 4: fill_params<4>(pl, N, best_ops); break;
+        case 8: fill_params<8>(pl, N, best_ops); break;
+        case 16: fill_params<16>(pl, N, best_ops); break;
+        case 32: fill_params<32>(pl, N, best_ops); break;
+        case 64: fill_params<64>(pl, N, best_ops); break;
+        }
+    }
+    {
+        std::lock_guard<std::mutex> lk(g_plan_mu);
+        if (g_plans.size() > 256) g_plans.clear();
+        g_plans[key] = pl;
+    }
+    *out = pl;
+    return RSA_OK;
+}
+
+static int device_sms() {
+    int dev = 0, sms = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) return 0;
+    if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) return 0;
+    return sms;
+}
+
+static void keep_pool_memory() {
+    static std::once_flag once;
+    std::call_once(once, [] {
+        int dev = 0;
+        if (cudaGetDevice(&dev) != cudaSuccess) return;
+        cudaMemPool_t pool;
+        if (cudaDeviceGetDefaultMemPool(&pool, dev) != cudaSuccess) return;
+        uint64_t thr = ~0ull;
+        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    });
+}
+
+static int check_modulus(const uint32_t* n, int nbits) {
+    if (nbits < 2 || nbits > RSA_MAX_NBITS) return RSA_ERANGE;
+    const int s = (nbits + 31) / 32;
+    const int top = nbits - 32 * (s - 1);    // bits allowed in limb s-1, 1..32
+    if (top < 32 && (n[s - 1] >> top) != 0) return RSA_ERANGE;
+    if ((n[0] & 1u) == 0) return RSA_EEVEN;
+    bool small = (n[0] < 3);
+    for (int i = 1; i < s && small; i++)
+        if (n[i]) small = false;
+    if (small) return RSA_EEVEN;
+    return RSA_OK;
+}
+
+// enqueue one batch on `stream` (device pointers, validated arguments)
+static int enqueue(const Plan& pl, const uint32_t* base, uint32_t* out, size_t count, cudaStream_t stream) {
+    const int sms = device_sms();
+    if (!sms) return RSA_ECUDA;
+    if (pl.exp_zero) {
+        if (rsa_b200_fill_one(out, count, pl.s_io, sms, stream) != cudaSuccess) return RSA_ECUDA;
+        g_launches++;
+        return RSA_OK;
+    }
+    int grid = 0, block = 0;
+    size_t nthr = 0;
+    if (rsa_b200_grid(pl.S, sms, &grid, &block, &nthr) != cudaSuccess) return RSA_ECUDA;
+    keep_pool_memory();
+    void* table = nullptr;
+    const size_t tbytes = (size_t)pl.ntab * pl.S * sizeof(uint32_t) * nthr;
+    if (cudaMallocAsync(&table, tbytes, stream) != cudaSuccess) return RSA_ECUDA;
+    std::vector<unsigned char> params = pl.params;
+    patch(pl.S, params.data(), base, out, table, count);
+    cudaError_t e = rsa_b200_launch(pl.S, params.data(), sms, stream);
+    cudaFreeAsync(table, stream);
+    if (e != cudaSuccess) return RSA_ECUDA;
+    g_launches++;
+    return RSA_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* rsa_strerror(int status) {
+    switch (status) {
+    case RSA_OK: return "ok";
+    case RSA_EINVAL: return "invalid argument";
+    case RSA_ERANGE: return "value out of range";
+    case RSA_EEVEN: return "modulus must be odd and >= 3";
+    case RSA_ENOTPRIME: return "not prime";
+    case RSA_EEQUAL: return "primes must differ";
+    case RSA_ENOTCOPRIME: return "exponent not coprime with totient";
+    case RSA_ECHAR: return "unsupported character";
+    case RSA_EODD: return "odd-length message";
+    case RSA_ENOSPC: return "output capacity too small";
+    case RSA_EPACKET: return "invalid packet";
+    case RSA_EBADKEY: return "d*e != 1 (mod phi)";
+    case RSA_ECUDA: return "CUDA error";
+    default: return "unknown status";
+    }
+}
+
+int rsa_modexp_batch(const uint32_t* base, const uint32_t* exp, const uint32_t* n, int nbits, size_t count,
+                     uint32_t* out, void* stream) {
+    if (!exp || !n) return RSA_EINVAL;
+    int st = check_modulus(n, nbits);
+    if (st) return st;
+    if (count == 0) return RSA_OK;
+    if (!base || !out) return RSA_EINVAL;
+    const int s = (nbits + 31) / 32;
+    const size_t bytes = count * (size_t)s * sizeof(uint32_t);
+    if (bytes / count / sizeof(uint32_t) != (size_t)s) return RSA_EINVAL;
+    const char* b0 = (const char*)base;
+    const char* o0 = (const char*)out;
+    if (b0 != o0 && b0 < o0 + bytes && o0 < b0 + bytes) return RSA_EINVAL;   // partial overlap
+    Plan pl;
+    st = get_plan(exp, n, nbits, &pl);
+    if (st) return st;
+    return enqueue(pl, base, out, count, (cudaStream_t)stream);
+}
+
+int rsa_modexp_batch_host(const uint32_t* base_host, const uint32_t* exp, const uint32_t* n, int nbits,
+                          size_t count, uint32_t* out_host) {
+    if (!exp || !n) return RSA_EINVAL;
+    int st = check_modulus(n, nbits);
+    if (st) return st;
+    if (count == 0) return RSA_OK;
+    if (!base_host || !out_host) return RSA_EINVAL;
+    Plan pl;
+    st = get_plan(exp, n, nbits, &pl);
+    if (st) return st;
+    const int s = (nbits + 31) / 32;
+    const size_t row = (size_t)s * sizeof(uint32_t);
+    // chunking: up to 8 chunks of >= 64K packets, two streams ping-pong
+    size_t nch = count / 65536;
+    if (nch < 1) nch = 1;
+    if (nch > 8) nch = 8;
+    const size_t per = (count + nch - 1) / nch;
+    cudaStream_t ss[2];
+    if (cudaStreamCreateWithFlags(&ss[0], cudaStreamNonBlocking) != cudaSuccess) return RSA_ECUDA;
+    if (cudaStreamCreateWithFlags(&ss[1], cudaStreamNonBlocking) != cudaSuccess) {
+        cudaStreamDestroy(ss[0]);
+        return RSA_ECUDA;
+    }
+    keep_pool_memory();
+    uint32_t* dbuf[2] = {nullptr, nullptr};
+    int rc = RSA_OK;
+    for (int k = 0; k < 2 && rc == RSA_OK; k++)
+        if (cudaMallocAsync((void**)&dbuf[k], per * row, ss[k]) != cudaSuccess) rc = RSA_ECUDA;
+    for (size_t c = 0; c < nch && rc == RSA_OK; c++) {
+        const size_t lo = c * per;
+        if (lo >= count) break;
+        const size_t cnt = (lo + per <= count) ? per : count - lo;
+        cudaStream_t sc = ss[c & 1];
+        uint32_t* d = dbuf[c & 1];
+        if (cudaMemcpyAsync(d, base_host + lo * s, cnt * row, cudaMemcpyHostToDevice, sc) != cudaSuccess) {
+            rc = RSA_ECUDA;
+            break;
+        }
+        rc = enqueue(pl, d, d, cnt, sc);
+        if (rc) break;
+        if (cudaMemcpyAsync(out_host + lo * s, d, cnt * row, cudaMemcpyDeviceToHost, sc) != cudaSuccess)
+            rc = RSA_ECUDA;
+    }
+    for (int k = 0; k < 2; k++) {
+        if (dbuf[k]) cudaFreeAsync(dbuf[k], ss[k]);
+        if (cudaStreamSynchronize(ss[k]) != cudaSuccess) rc = RSA_ECUDA;
+        cudaStreamDestroy(ss[k]);
+    }
+    return rc;
+}
+
+int rsa_plan_info(const uint32_t* exp, const uint32_t* n, int nbits, rsa_plan_info_t* info) {
+    if (!exp || !n || !info) return RSA_EINVAL;
+    int st = check_modulus(n, nbits);
+    if (st) return st;
+    Plan pl;
+    st = get_plan(exp, n, nbits, &pl);
+    if (st) return st;
+    memset(info, 0, sizeof(*info));
+    info->width_class = pl.S;
+    info->s_io = pl.s_io;
+    info->window = pl.window;
+    info->table_entries = pl.ntab;
+    info->nops = pl.nops;
+    info->montmuls = pl.montmuls;
+    info->squarings = pl.squarings;
+    info->exp_bits = pl.exp_bits;
+    const int sms = device_sms();
+    if (sms) {
+        size_t nthr;
+        rsa_b200_grid(pl.S, sms, &info->grid, &info->block, &nthr);
+    }
+    return RSA_OK;
+}
+
+int rsa_set_window(int w) {
+    if (w < 0 || w > 7) return RSA_EINVAL;
+    t_window_override = w;
+    return RSA_OK;
+}
+
+unsigned long long rsa_kernel_launches(void) { return g_launches.load(); }
+
+// ------------------------------------------------------------------ Fig 1
+
+int rsa_keygen_check(const uint32_t* p, const uint32_t* q, int pq_limbs, const uint32_t* e, int e_limbs,
+                     uint32_t* n_out, uint32_t* phi_out, uint32_t* d_out) {
+    if (!p || !q || !e || !n_out || !phi_out || !d_out) return RSA_EINVAL;
+    if (pq_limbs < 1 || pq_limbs > 64 || e_limbs < 1 || e_limbs > 128) return RSA_EINVAL;
+    BN P = rsa_host::from_limbs(p, pq_limbs), Q = rsa_host::from_limbs(q, pq_limbs);
+    BN E = rsa_host::from_limbs(e, e_limbs);
+    if (!rsa_host::is_probable_prime(P) || !rsa_host::is_probable_prime(Q)) return RSA_ENOTPRIME;
+    if (rsa_host::cmp(P, Q) == 0) return RSA_EEQUAL;
+    BN one{1u};
+    BN N = rsa_host::mul(P, Q);
+    BN PHI = rsa_host::mul(rsa_host::sub(P, one), rsa_host::sub(Q, one));
+    rsa_host::to_limbs(N, n_out, 2 * pq_limbs);
+    rsa_host::to_limbs(PHI, phi_out, 2 * pq_limbs);
+    if (rsa_host::cmp(E, one) <= 0 || rsa_host::cmp(E, PHI) >= 0) return RSA_ERANGE;
+    if (!rsa_host::is_one(rsa_host::gcd(PHI, E))) return RSA_ENOTCOPRIME;
+    BN D;
+    if (!rsa_host::inverse(E, PHI, &D)) return RSA_ENOTCOPRIME;
+    rsa_host::to_limbs(D, d_out, 2 * pq_limbs);
+    return RSA_OK;
+}
+
+int rsa_validate_key(const uint32_t* e, const uint32_t* d, const uint32_t* p, const uint32_t* q, int limbs,
+                     uint32_t* residue_out) {
+    if (!e || !d || !p || !q || !residue_out || limbs < 1 || limbs > 64) return RSA_EINVAL;
+    BN one{1u};
+    BN PHI = rsa_host::mul(rsa_host::sub(rsa_host::from_limbs(p, limbs), one),
+                           rsa_host::sub(rsa_host::from_limbs(q, limbs), one));
+    if (PHI.empty()) return RSA_EINVAL;
+    BN R = rsa_host::mod(rsa_host::mul(rsa_host::from_limbs(d, limbs), rsa_host::from_limbs(e, limbs)), PHI);
+    rsa_host::to_limbs(R, residue_out, 2 * limbs);
+    return rsa_host::is_one(R) ? RSA_OK : RSA_EBADKEY;
+}
+
+// ------------------------------------------------------------------ sec. 2 codec
+
+int rsa_encode(const char* text, uint32_t* packets, size_t cap, size_t* count_out) {
+    if (!text || !count_out || (!packets && cap)) return RSA_EINVAL;
+    size_t letters = 0;
+    for (size_t i = 0; text[i]; i++) {
+        const char c = text[i];
+        if (c == ' ') continue;
+        if (c < 'a' || c > 'z') {
+            *count_out = i;
+            return RSA_ECHAR;
+        }
+        letters++;
+    }
+    if (letters & 1) return RSA_EODD;
+    if (letters / 2 > cap) {
+        *count_out = letters / 2;
+        return RSA_ENOSPC;
+    }
+    size_t k = 0;
+    int half = -1;
+    for (size_t i = 0; text[i]; i++) {
+        if (text[i] == ' ') continue;
+        const int v = text[i] - 'a';
+        if (half < 0) {
+            half = v;
+        } else {
+            packets[k++] = (uint32_t)(100 * half + v);
+            half = -1;
+        }
+    }
+    *count_out = k;
+    return RSA_OK;
+}
+
+int rsa_decode(const uint32_t* packets, size_t count, char* text, size_t cap) {
+    if (!text || (!packets && count)) return RSA_EINVAL;
+    if (cap < 2 * count + 1) return RSA_ENOSPC;
+    for (size_t i = 0; i < count; i++) {
+        const uint32_t hi = packets[i] / 100, lo = packets[i] % 100;
+        if (hi > 25 || lo > 25) return RSA_EPACKET;
+        text[2 * i] = (char)('a' + hi);
+        text[2 * i + 1] = (char)('a' + lo);
+    }
+    text[2 * count] = '\0';
+    return RSA_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,92 @@
+"""The C-ABI library loads and exports every symbol include/rsa_b200.h declares
+(no GPU needed); host-only calls (keygen check, codec) work and agree with the
+oracle / the paper."""
+import json
+import os
+import re
+import subprocess
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+HEADER = os.path.join(ROOT, "include", "rsa_b200.h")
+GOLD = os.path.join(ROOT, "tests", "golden")
+
+
+def declared():
+    src = open(HEADER).read()
+    return sorted(set(re.findall(r"^\s*(?:const\s+)?[\w\s\*]+?\b(rsa_\w+)\s*\(", src, re.M)))
+
+
+def test_header_declares_the_north_star_calls():
+    names = declared()
+    for fn in ["rsa_keygen_check", "rsa_modexp_batch", "rsa_encode", "rsa_decode", "rsa_strerror"]:
+        assert fn in names
+
+
+def test_library_exports_every_declared_symbol():
+    import paper_1407_1465_b200 as R
+    out = subprocess.check_output(["nm", "-D", "--defined-only", R.LIB_PATH], text=True)
+    exported = set(l.split()[-1] for l in out.splitlines() if " T " in l)
+    for fn in declared():
+        assert fn in exported, fn
+        getattr(R._lib, fn)
+    assert set(R.EXPORTS) <= exported
+
+
+def test_library_is_sm100a():
+    import paper_1407_1465_b200 as R
+    out = subprocess.check_output(["/usr/local/cuda/bin/cuobjdump", "--list-elf", R.LIB_PATH], text=True)
+    assert "sm_100a" in out
+
+
+def test_host_keygen_matches_oracle_and_paper():
+    import oracle
+    import paper_1407_1465_b200 as R
+    import workload
+    fig2 = json.load(open(os.path.join(GOLD, "fig2_key.json")))
+    assert R.rsa_keygen_check(fig2["p"], fig2["q"], fig2["e"]) == (fig2["n"], fig2["phi"], fig2["d"])
+    assert R.rsa_validate_key(131, 137, 131, 137) == (False, 267)
+    assert R.rsa_validate_key(131, 14171, 131, 137) == (True, 1)
+    for name in ["toy17947", "table2_513581", "rsa64", "rsa96", "rsa512", "rsa1024", "rsa2048"]:
+        k = workload.key(name)
+        assert R.rsa_keygen_check(k["p"], k["q"], k["e"]) == oracle.keygen_check(k["p"], k["q"], k["e"])
+
+
+@pytest.mark.parametrize("args,code", [((13, 13, 3), -5), ((15, 17, 3), -4), ((17, 11, 2), -6),
+                                       ((17, 11, 1), -2), ((17, 11, 160), -2), ((1005, 509, 131), -4),
+                                       ((561, 11, 3), -4)])
+def test_host_keygen_errors(args, code):
+    import paper_1407_1465_b200 as R
+    with pytest.raises(R.RsaError) as ei:
+        R.rsa_keygen_check(*args)
+    assert ei.value.code == code
+
+
+def test_codec_matches_paper_and_oracle():
+    import oracle
+    import paper_1407_1465_b200 as R
+    g = json.load(open(os.path.join(GOLD, "sec2_packets.json")))
+    assert R.rsa_encode(g["text"]) == g["packets"] == oracle.encode(g["text"])
+    assert R.rsa_decode(g["packets"]) == g["decoded"]
+    for bad, code in [("a", R.RSA_EODD), ("aB", R.RSA_ECHAR)]:
+        with pytest.raises(R.RsaError) as ei:
+            R.rsa_encode(bad)
+        assert ei.value.code == code
+    with pytest.raises(R.RsaError) as ei:
+        R.rsa_decode([2600])
+    assert ei.value.code == R.RSA_EPACKET
+
+
+def test_plan_montmul_counts():
+    """Host plan: e=65537 costs 19 montmuls (16 S + 1 M + 2 conversions,
+    SURVEY.md sec. 8 table); windowed plans never cost more than binary."""
+    import paper_1407_1465_b200 as R
+    import workload
+    k = workload.key("rsa2048")
+    p = R.rsa_plan_info(65537, k["n"], 2048)
+    assert p["montmuls"] == 19 and p["squarings"] == 16 and p["width_class"] == 64
+    pd = R.rsa_plan_info(k["d"], k["n"], 2048)
+    bits, pop = k["d"].bit_length(), bin(k["d"]).count("1")
+    assert pd["montmuls"] < (bits - 1) + (pop - 1) + 2          # beats Fig 5 binary
+    assert pd["squarings"] >= bits - 1 - pd["window"]

@@ -1,0 +1,110 @@
+"""Design check of the kernel's carry scheme (paper_1407_1465_b200/csrc/mont.cuh)
+on CPU: a bit-exact Python model of cios_step/montmul -- register arrays X, Y,
+`hi`, the PTX carry flag -- compared with the plain definition
+a*b*R^-1 mod n (Python ints).  This pins the even/odd + pre-shift fold
+bookkeeping before any GPU run; the GPU parity tests then pin the kernel."""
+import random
+
+import pytest
+
+M32 = 0xFFFFFFFF
+
+
+class CC:
+    """PTX carry flag semantics for add.cc/addc/mad*.cc."""
+    def __init__(self):
+        self.c = 0
+
+    def add_cc(self, a, b, cin=0):
+        s = a + b + cin
+        self.c = s >> 32
+        return s & M32
+
+    def mad_lo_cc(self, a, b, c, cin=0):
+        return self.add_cc((a * b) & M32, c, cin)
+
+    def mad_hi_cc(self, a, b, c, cin=0):
+        return self.add_cc((a * b) >> 32, c, cin)
+
+
+def cios_step(X, Y, hi, a, b, n, n0inv):
+    S = len(a)
+    cc = CC()
+    X[0] = cc.add_cc(X[0], Y[1])
+    for j in range(1, S - 2, 2):
+        c = cc.c; Y[j - 1] = cc.mad_lo_cc(a[j], b, Y[j + 1], c)
+        c = cc.c; Y[j] = cc.mad_hi_cc(a[j], b, Y[j + 2], c)
+    c = cc.c; Y[S - 2] = cc.mad_lo_cc(a[S - 1], b, 0, c)
+    c = cc.c; Y[S - 1] = cc.mad_hi_cc(a[S - 1], b, hi, c)
+    hi = cc.c
+    X[0] = cc.mad_lo_cc(a[0], b, X[0])
+    c = cc.c; X[1] = cc.mad_hi_cc(a[0], b, X[1], c)
+    for j in range(2, S, 2):
+        c = cc.c; X[j] = cc.mad_lo_cc(a[j], b, X[j], c)
+        c = cc.c; X[j + 1] = cc.mad_hi_cc(a[j], b, X[j + 1], c)
+    c = cc.c; Y[S - 1] = cc.add_cc(Y[S - 1], 0, c)
+    hi = hi + cc.c
+    m = (X[0] * n0inv) & M32
+    Y[0] = cc.mad_lo_cc(n[1], m, Y[0])
+    c = cc.c; Y[1] = cc.mad_hi_cc(n[1], m, Y[1], c)
+    for j in range(3, S, 2):
+        c = cc.c; Y[j - 1] = cc.mad_lo_cc(n[j], m, Y[j - 1], c)
+        c = cc.c; Y[j] = cc.mad_hi_cc(n[j], m, Y[j], c)
+    hi = hi + cc.c
+    X[0] = cc.mad_lo_cc(n[0], m, X[0])
+    assert X[0] == 0
+    c = cc.c; X[1] = cc.mad_hi_cc(n[0], m, X[1], c)
+    for j in range(2, S, 2):
+        c = cc.c; X[j] = cc.mad_lo_cc(n[j], m, X[j], c)
+        c = cc.c; X[j + 1] = cc.mad_hi_cc(n[j], m, X[j + 1], c)
+    c = cc.c; Y[S - 1] = cc.add_cc(Y[S - 1], 0, c)
+    hi = hi + cc.c
+    assert hi < 2**32
+    return hi
+
+
+def montmul_model(a, b, n, S):
+    n0inv = (-pow(n[0], -1, 2**32)) % 2**32
+    X, Y, hi = [0] * S, [0] * S, 0
+    for i in range(S):
+        if i % 2 == 0:
+            hi = cios_step(X, Y, hi, a, b[i], n, n0inv)
+        else:
+            hi = cios_step(Y, X, hi, a, b[i], n, n0inv)
+    cc = CC()
+    X[0] = cc.add_cc(X[0], Y[1])
+    for k in range(1, S - 1):
+        c = cc.c; X[k] = cc.add_cc(X[k], Y[k + 1], c)
+    c = cc.c; X[S - 1] = cc.add_cc(X[S - 1], 0, c)
+    hi = hi + cc.c
+    r = sum(v << (32 * k) for k, v in enumerate(X)) + (hi << (32 * S))
+    N = sum(v << (32 * k) for k, v in enumerate(n))
+    return r - N if r >= N else r
+
+
+def L(x, S):
+    return [(x >> (32 * k)) & M32 for k in range(S)]
+
+
+@pytest.mark.parametrize("S", [2, 4, 8, 16])
+def test_cios_model_random(S):
+    rnd = random.Random(S)
+    R = 1 << (32 * S)
+    for _ in range(300):
+        N = rnd.getrandbits(32 * S) | 1 | (rnd.choice([1, 0]) << (32 * S - 1))
+        if N < 3:
+            continue
+        A = rnd.randrange(R)                  # a < R (to-Montgomery case)
+        B = rnd.randrange(N)
+        got = montmul_model(L(A, S), L(B, S), L(N, S), S)
+        assert got == (A * B * pow(R, -1, N)) % N
+
+
+@pytest.mark.parametrize("S", [2, 4, 8])
+def test_cios_model_extremes(S):
+    R = 1 << (32 * S)
+    for N in [R - 1, R - 3, (R >> 1) + 1, 3, 0xFFFFFFFF, (R >> 1) | 1]:
+        for A in [0, 1, N - 1, R - 1, N // 2]:
+            for B in [0, 1, N - 1, N // 2]:
+                got = montmul_model(L(A, S), L(B, S), L(N, S), S)
+                assert got == (A * B * pow(R, -1, N)) % N, (N, A, B)
