@@ -49,6 +49,7 @@ def parse():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", default="rsa2048-roundtrip", choices=sorted(WORKLOADS))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--count", type=int, default=0, help="override packets per rank (profiling only)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=15.0, help="CPU-seconds budget of the oracle sample")
@@ -116,10 +117,10 @@ def cpu_baseline(key: dict, base: np.ndarray, legs, cpu_seconds: float):
     bounded sample of the same workload: the first `k` packets, every leg."""
     import oracle
     cores = os.cpu_count() or 1
-    # calibrate one packet of the most expensive leg
+    # calibrate on 2 random (non-edge) packets of the most expensive leg
     t0 = time.perf_counter()
-    oracle.modexp_batch(base[:1], key[legs[-1][1]], key["n"], nthreads=1)
-    per = max(time.perf_counter() - t0, 1e-6) * len(legs)
+    oracle.modexp_batch(base[16:18], key[legs[-1][1]], key["n"], nthreads=1)
+    per = max(time.perf_counter() - t0, 1e-6) / 2 * len(legs)
     k = int(max(cores, min(len(base), cpu_seconds / per)))
     k = min(k, len(base))
     t0 = time.perf_counter()
@@ -132,15 +133,17 @@ def cpu_baseline(key: dict, base: np.ndarray, legs, cpu_seconds: float):
                       f"({', '.join(l for l, _ in legs)}); {wall:.1f} s wall on {cores} threads"}
 
 
-def ncu_traffic(config: str):
-    """dram bytes per launch of the dominant kernel from the committed ncu
-    --set full summary (profiles/), or None."""
+def ncu_traffic(leg: str, count: int):
+    """DRAM bytes (read + write) per launch of the dominant kernel, from the
+    committed ncu --set full capture (profiles/ncu_traffic.json, bytes per
+    packet) scaled to this launch's packets; None if not captured."""
     path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     try:
         with open(path) as f:
-            return json.load(f).get(config)
+            rec = json.load(f).get(leg)
     except (OSError, ValueError):
         return None
+    return None if not rec else rec["bytes_per_packet"] * count
 
 
 # ------------------------------------------------------------------ arms
@@ -156,8 +159,8 @@ def run_reference(args, rank, world):
     import oracle
     cores = os.cpu_count() or 1
     t0 = time.perf_counter()
-    oracle.modexp_batch(base[:1], key[legs[-1][1]], key["n"], nthreads=1)
-    per = max(time.perf_counter() - t0, 1e-6) * len(legs)
+    oracle.modexp_batch(base[16:18], key[legs[-1][1]], key["n"], nthreads=1)
+    per = max(time.perf_counter() - t0, 1e-6) / 2 * len(legs)
     budget = 120.0 / max(1, args.steps + args.warmup)          # whole run within a few minutes
     k = int(min(count, max(cores, budget * cores / per)))
     times = []
@@ -189,6 +192,8 @@ def run_ours(args, rank, world, local_rank):
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
     key_name, count, legs = WORKLOADS[args.config]
+    if args.count:
+        count = args.count
     key = workload.key(key_name)
     nb, n = key["nbits"], key["n"]
     s = workload.limbs_needed(nb)
@@ -285,7 +290,8 @@ def run_ours(args, rank, world, local_rank):
     achieved = products / (leg_ms[dom] / 1e3) / 1e12
     peak = R_PRODUCTS_PER_CLK_PER_SM * sms * f_max * 1e6 / 1e12
     roofline = {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "Tprod/s", "frac": achieved / peak,
-                "traffic": ncu_traffic(args.config),
+                "traffic": ncu_traffic(legs[dom][0], count),
+                "traffic_unit": "bytes per launch", "algorithmic_bytes": count * s * 4 * 2,
                 "kernel": f"modexp_kernel<{S}> ({legs[dom][0]})",
                 "algorithmic": f"{plans[dom]['montmuls']} montmul/packet x (2S^2+S = {prod_per_mm}) 32x32->64 "
                                f"limb products x {count} packets per launch",
