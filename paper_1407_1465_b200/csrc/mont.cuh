@@ -139,13 +139,19 @@ __device__ __forceinline__ void montmul(uint32_t (&a)[S], const typename BVec<S>
             }
         }
     } else {
+        // 8 CIOS iterations per loop trip: with 4 per trip ptxas permutes the
+        // rotated X/Y registers at the back edge with IMAD.MOV / XOR swaps
+        // (fmaheavy slots); with 8 it allocates them in place.
 #pragma unroll 1
-        for (int g = 0; g < S / G; g++) {
-            const typename BVec<S>::T bv = bslot[g * stride];
-            cios_step<S>(X, Y, hi, a, bv.x, n, n0inv);
-            cios_step<S>(Y, X, hi, a, bv.y, n, n0inv);
-            cios_step<S>(X, Y, hi, a, bv.z, n, n0inv);
-            cios_step<S>(Y, X, hi, a, bv.w, n, n0inv);
+        for (int g0 = 0; g0 < S / G; g0 += 2) {
+#pragma unroll
+            for (int g = g0; g < g0 + 2; g++) {
+                const typename BVec<S>::T bv = bslot[g * stride];
+                cios_step<S>(X, Y, hi, a, bv.x, n, n0inv);
+                cios_step<S>(Y, X, hi, a, bv.y, n, n0inv);
+                cios_step<S>(X, Y, hi, a, bv.z, n, n0inv);
+                cios_step<S>(Y, X, hi, a, bv.w, n, n0inv);
+            }
         }
     }
 
