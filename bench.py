@@ -37,6 +37,8 @@ WORKLOADS = {
     "rsa2048-roundtrip": ("rsa2048", 1 << 20, [("enc_e65537", "e"), ("dec_full_d", "d")]),
     "rsa2048-enc": ("rsa2048", 1 << 20, [("enc_e65537", "e")]),
     "rsa2048-dec": ("rsa2048", 1 << 20, [("dec_full_d", "d")]),
+    "rsa4096-dec": ("rsa4096", 256 << 10, [("dec_full_d", "d")]),
+    "rsa4096-roundtrip": ("rsa4096", 256 << 10, [("enc_e65537", "e"), ("dec_full_d", "d")]),
     "u64-roundtrip": ("rsa64", 16 << 20, [("enc_e65537", "e"), ("dec_full_d", "d")]),
     "toy-roundtrip": ("toy17947", 9, [("enc_e131", "e"), ("dec_d14171", "d")]),
 }
@@ -133,14 +135,14 @@ def cpu_baseline(key: dict, base: np.ndarray, legs, cpu_seconds: float):
                       f"({', '.join(l for l, _ in legs)}); {wall:.1f} s wall on {cores} threads"}
 
 
-def ncu_traffic(leg: str, count: int):
+def ncu_traffic(key_name: str, leg: str, count: int):
     """DRAM bytes (read + write) per launch of the dominant kernel, from the
     committed ncu --set full capture (profiles/ncu_traffic.json, bytes per
     packet) scaled to this launch's packets; None if not captured."""
     path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     try:
         with open(path) as f:
-            rec = json.load(f).get(leg)
+            rec = json.load(f).get(key_name, {}).get(leg)
     except (OSError, ValueError):
         return None
     return None if not rec else rec["bytes_per_packet"] * count
@@ -290,9 +292,9 @@ def run_ours(args, rank, world, local_rank):
     achieved = products / (leg_ms[dom] / 1e3) / 1e12
     peak = R_PRODUCTS_PER_CLK_PER_SM * sms * f_max * 1e6 / 1e12
     roofline = {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "Tprod/s", "frac": achieved / peak,
-                "traffic": ncu_traffic(legs[dom][0], count),
+                "traffic": ncu_traffic(key_name, legs[dom][0], count),
                 "traffic_unit": "bytes per launch", "algorithmic_bytes": count * s * 4 * 2,
-                "kernel": f"modexp_kernel<{S}> ({legs[dom][0]})",
+                "kernel": (f"modexp_pair_kernel<{S}>" if S == 128 else f"modexp_kernel<{S}>") + f" ({legs[dom][0]})",
                 "algorithmic": f"{plans[dom]['montmuls']} montmul/packet x (2S^2+S = {prod_per_mm}) 32x32->64 "
                                f"limb products x {count} packets per launch",
                 "peak_basis": f"{R_PRODUCTS_PER_CLK_PER_SM} products/clk/SM (IMAD.WIDE half rate, "

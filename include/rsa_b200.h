@@ -6,7 +6,7 @@
  * data-parallel hot path -- C = M^e mod n for encryption and M = C^d mod n
  * for decryption, applied independently to every packet (sec. 2;
  * PAPER.md:65, sec. 3.3; sec. 11) -- for moduli from the
- * paper's toy key (n = 17947) to 2048-bit keys, plus the key-generation check
+ * paper's toy key (n = 17947) to 4096-bit keys, plus the key-generation check
  * of Fig 1 and the packetisation of sec. 2.
  *
  * Conventions for every call:
@@ -32,7 +32,7 @@ extern "C" {
 /* ---- status codes ---------------------------------------------------- */
 #define RSA_OK            0
 #define RSA_EINVAL       -1   /* null pointer, bad size/length argument, partial overlap */
-#define RSA_ERANGE       -2   /* nbits out of [2, 2048], n >= 2^nbits, or e not in (1, phi) */
+#define RSA_ERANGE       -2   /* nbits out of [2, 4096], n >= 2^nbits, or e not in (1, phi) */
 #define RSA_EEVEN        -3   /* modulus even or < 3 (Montgomery needs gcd(n, 2) = 1) */
 #define RSA_ENOTPRIME    -4   /* p or q not prime (Fig 1: "random prime numbers") */
 #define RSA_EEQUAL       -5   /* p == q (Fig 1: "two different ... prime numbers") */
@@ -45,7 +45,7 @@ extern "C" {
 #define RSA_ECUDA       -12   /* CUDA launch / allocation / copy failure */
 
 /* Largest modulus the GPU path accepts in this build (bits). */
-#define RSA_MAX_NBITS 2048
+#define RSA_MAX_NBITS 4096
 
 const char* rsa_strerror(int status);
 

@@ -26,7 +26,7 @@ LIB_PATH = os.path.join(_HERE, "librsa_b200.so")
 RSA_OK, RSA_EINVAL, RSA_ERANGE, RSA_EEVEN = 0, -1, -2, -3
 RSA_ENOTPRIME, RSA_EEQUAL, RSA_ENOTCOPRIME = -4, -5, -6
 RSA_ECHAR, RSA_EODD, RSA_ENOSPC, RSA_EPACKET, RSA_EBADKEY, RSA_ECUDA = -7, -8, -9, -10, -11, -12
-RSA_MAX_NBITS = 2048
+RSA_MAX_NBITS = 4096
 
 EXPORTS = ["rsa_strerror", "rsa_keygen_check", "rsa_validate_key", "rsa_modexp_batch",
            "rsa_modexp_batch_host", "rsa_plan_info", "rsa_set_window", "rsa_encode", "rsa_decode",

@@ -17,6 +17,7 @@
 #include <stdint.h>
 
 #include "mont.cuh"
+#include "mont_pair.cuh"
 #include "plan.h"
 
 namespace rsa_b200 {
@@ -119,6 +120,134 @@ modexp_kernel(const __grid_constant__ ModexpParams<S> p) {
     }
 }
 
+
+// ---------------------------------------------------------------------------
+// S = 2L limbs (4096-bit class): two lanes per packet (mont_pair.cuh).  Every
+// thread runs the same number of trips so each warp stays converged (the
+// pair shuffles use the full mask); out-of-range trips recompute the last
+// packet and skip the store.
+template <int S>
+__global__ void __launch_bounds__(128, 2)
+modexp_pair_kernel(const __grid_constant__ ModexpParams<S> p) {
+    constexpr int L = S / 2;
+    constexpr int NG = S / 4;         // uint4 groups per packet
+    constexpr int NGL = L / 4;        // groups per lane
+    constexpr int NQ = L / 8;         // uint4 of odd (even) limbs per lane
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    uint4* const nodd_all = reinterpret_cast<uint4*>(smem_raw);
+    uint4* const neven_all = nodd_all + 2 * NQ;
+    uint4* const slots = neven_all + 2 * NQ;
+    const int ppb = blockDim.x / 2;
+    for (int i = threadIdx.x; i < 2 * NQ; i += blockDim.x) {
+        const int h = i / NQ, q = i % NQ, o = h * L + 8 * q;
+        nodd_all[i] = make_uint4(p.n[o + 1], p.n[o + 3], p.n[o + 5], p.n[o + 7]);
+        neven_all[i] = make_uint4(p.n[o], p.n[o + 2], p.n[o + 4], p.n[o + 6]);
+    }
+    __syncthreads();
+    const int half = threadIdx.x & 1;
+    const int pk = threadIdx.x >> 1;
+    const uint4* nodd4 = nodd_all + half * NQ;
+    const uint4* neven4 = neven_all + half * NQ;
+    uint4* const bslot = slots + pk;
+    const unsigned gpk = (blockIdx.x * blockDim.x + threadIdx.x) >> 1;
+    const unsigned npk = (gridDim.x * blockDim.x) >> 1;
+    uint4* const table = reinterpret_cast<uint4*>(p.table);
+    const unsigned long long trips = (p.count + npk - 1) / npk;
+
+    for (unsigned long long t = 0; t < trips; t++) {
+        const unsigned long long pkt0 = gpk + t * npk;
+        const bool valid = pkt0 < p.count;
+        const unsigned long long pkt = valid ? pkt0 : p.count - 1;
+        uint32_t a[L];
+        const uint32_t* src = p.base + pkt * (unsigned long long)p.s_io;
+        if (p.s_io == S) {
+#pragma unroll
+            for (int k = 0; k < L; k += 4) {
+                const uint4 v = __ldg(reinterpret_cast<const uint4*>(src + half * L + k));
+                a[k] = v.x; a[k + 1] = v.y; a[k + 2] = v.z; a[k + 3] = v.w;
+            }
+        } else {
+#pragma unroll
+            for (int k = 0; k < L; k++) a[k] = (half * L + k < p.s_io) ? __ldg(src + half * L + k) : 0u;
+        }
+        for (int i = 0; i < p.nops; i++) {
+            const RsaOp op = p.ops[i];
+            if (op.flags & RSA_F_LOADA) {
+#pragma unroll
+                for (int g = 0; g < NGL; g++) {
+                    const uint4 v = table[((size_t)op.lidx * NG + half * NGL + g) * npk + gpk];
+                    a[4 * g] = v.x; a[4 * g + 1] = v.y; a[4 * g + 2] = v.z; a[4 * g + 3] = v.w;
+                }
+            }
+            for (int r = 0; r < op.rep; r++) {
+                __syncwarp();
+                if (op.kind == RSA_OP_SQR) {
+#pragma unroll
+                    for (int g = 0; g < NGL; g++)
+                        bslot[(half * NGL + g) * ppb] = make_uint4(a[4 * g], a[4 * g + 1], a[4 * g + 2], a[4 * g + 3]);
+                } else if (op.kind == RSA_OP_MUL) {
+#pragma unroll
+                    for (int g = 0; g < NGL; g++)
+                        bslot[(half * NGL + g) * ppb] = table[((size_t)op.bidx * NG + half * NGL + g) * npk + gpk];
+                } else if (op.kind == RSA_OP_R2) {
+#pragma unroll
+                    for (int g = 0; g < NGL; g++) {
+                        const int o = half * L + 4 * g;
+                        bslot[(half * NGL + g) * ppb] = make_uint4(p.r2[o], p.r2[o + 1], p.r2[o + 2], p.r2[o + 3]);
+                    }
+                } else {
+#pragma unroll
+                    for (int g = 0; g < NGL; g++)
+                        bslot[(half * NGL + g) * ppb] = make_uint4((half == 0 && g == 0) ? 1u : 0u, 0u, 0u, 0u);
+                }
+                __syncwarp();
+                montmul_pair<L>(a, bslot, ppb, nodd4, neven4, p.n0inv, half);
+            }
+            if (op.flags & RSA_F_STORE) {
+#pragma unroll
+                for (int g = 0; g < NGL; g++)
+                    table[((size_t)op.sidx * NG + half * NGL + g) * npk + gpk] =
+                        make_uint4(a[4 * g], a[4 * g + 1], a[4 * g + 2], a[4 * g + 3]);
+            }
+        }
+        if (valid) {
+            uint32_t* dst = p.out + pkt * (unsigned long long)p.s_io;
+            if (p.s_io == S) {
+#pragma unroll
+                for (int k = 0; k < L; k += 4)
+                    *reinterpret_cast<uint4*>(dst + half * L + k) = make_uint4(a[k], a[k + 1], a[k + 2], a[k + 3]);
+            } else {
+#pragma unroll
+                for (int k = 0; k < L; k++)
+                    if (half * L + k < p.s_io) dst[half * L + k] = a[k];
+            }
+        }
+    }
+}
+
+template <int S>
+static cudaError_t launch_pair(const void* params, int sms, cudaStream_t stream, int* grid_out,
+                               int* block_out, size_t* slots_out, bool query_only) {
+    const int block = 128;
+    const size_t smem = sizeof(uint4) * (4 * (S / 16) + (S / 4) * (block / 2));
+    static int occ = -1;
+    if (occ < 0) {
+        cudaError_t e = cudaFuncSetAttribute(modexp_pair_kernel<S>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)smem);
+        if (e != cudaSuccess) return e;
+        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, modexp_pair_kernel<S>, block, smem);
+        if (e != cudaSuccess) return e;
+        if (occ < 1) occ = 1;
+    }
+    const int grid = sms * occ;
+    if (grid_out) *grid_out = grid;
+    if (block_out) *block_out = block;
+    if (slots_out) *slots_out = (size_t)grid * block / 2;
+    if (query_only) return cudaSuccess;
+    modexp_pair_kernel<S><<<grid, block, smem, stream>>>(*static_cast<const ModexpParams<S>*>(params));
+    return cudaGetLastError();
+}
+
 // exp == 0: every output is 1 mod n = 1 (n >= 3), reading Z12
 __global__ void fill_one_kernel(uint32_t* out, unsigned long long count, int s_io) {
     const unsigned long long total = count * (unsigned long long)s_io;
@@ -163,11 +292,13 @@ cudaError_t rsa_b200_launch(int S, const void* params, int sms, cudaStream_t str
     case 16: return launch_class<16>(params, sms, stream, nullptr, nullptr, nullptr, false);
     case 32: return launch_class<32>(params, sms, stream, nullptr, nullptr, nullptr, false);
     case 64: return launch_class<64>(params, sms, stream, nullptr, nullptr, nullptr, false);
+    case 128: return launch_pair<128>(params, sms, stream, nullptr, nullptr, nullptr, false);
     default: return cudaErrorInvalidValue;
     }
 }
 
-// threads of the persistent grid for class S (sizes the table workspace)
+// per-packet table slots of the persistent grid for class S (threads, or
+// lane pairs for S = 128): sizes the table workspace
 cudaError_t rsa_b200_grid(int S, int sms, int* grid, int* block, size_t* nthreads) {
     using namespace rsa_b200;
     switch (S) {
@@ -177,6 +308,7 @@ cudaError_t rsa_b200_grid(int S, int sms, int* grid, int* block, size_t* nthread
     case 16: return launch_class<16>(nullptr, sms, 0, grid, block, nthreads, true);
     case 32: return launch_class<32>(nullptr, sms, 0, grid, block, nthreads, true);
     case 64: return launch_class<64>(nullptr, sms, 0, grid, block, nthreads, true);
+    case 128: return launch_pair<128>(nullptr, sms, 0, grid, block, nthreads, true);
     default: return cudaErrorInvalidValue;
     }
 }
@@ -190,6 +322,7 @@ size_t rsa_b200_params_size(int S) {
     case 16: return sizeof(ModexpParams<16>);
     case 32: return sizeof(ModexpParams<32>);
     case 64: return sizeof(ModexpParams<64>);
+    case 128: return sizeof(ModexpParams<128>);
     default: return 0;
     }
 }

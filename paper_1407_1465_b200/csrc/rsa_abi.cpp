@@ -74,7 +74,7 @@ struct Plan {
 };
 
 static int width_class(int s_io) {
-    static const int classes[] = {2, 4, 8, 16, 32, 64};
+    static const int classes[] = {2, 4, 8, 16, 32, 64, 128};
     for (int c : classes)
         if (s_io <= c) return c;
     return 0;
@@ -163,6 +163,7 @@ static void patch(int S, void* raw, const uint32_t* base, uint32_t* out, void* t
     case 16: patch_params<16>(raw, base, out, table, count); break;
     case 32: patch_params<32>(raw, base, out, table, count); break;
     case 64: patch_params<64>(raw, base, out, table, count); break;
+    case 128: patch_params<128>(raw, base, out, table, count); break;
     }
 }
 
@@ -220,6 +221,7 @@ static int get_plan(const uint32_t* exp, const uint32_t* n, int nbits, Plan* out
         case 16: fill_params<16>(pl, N, best_ops); break;
         case 32: fill_params<32>(pl, N, best_ops); break;
         case 64: fill_params<64>(pl, N, best_ops); break;
+        case 128: fill_params<128>(pl, N, best_ops); break;
         }
     }
     {

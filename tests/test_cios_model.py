@@ -108,3 +108,101 @@ def test_cios_model_extremes(S):
             for B in [0, 1, N - 1, N // 2]:
                 got = montmul_model(L(A, S), L(B, S), L(N, S), S)
                 assert got == (A * B * pow(R, -1, N)) % N, (N, A, B)
+
+
+# ---------------------------------------------------------------- lane-pair (S = 2L) scheme
+
+def cios_step_pair(st, a, b, n, n0inv, L):
+    """Both lanes run cios_step on their halves; lane 0's m is broadcast; lane
+    1's dropped low word moves to lane 0's top (mont_pair.cuh)."""
+    # products on each lane; m from lane 0
+    X0, Y0, h0 = st[0]
+    X1, Y1, h1 = st[1]
+    out = []
+    ms = []
+    for lane in (0, 1):
+        X, Y, hi = st[lane]
+        cc = CC()
+        X[0] = cc.add_cc(X[0], Y[1])
+        for j in range(1, L - 2, 2):
+            c = cc.c; Y[j - 1] = cc.mad_lo_cc(a[lane][j], b, Y[j + 1], c)
+            c = cc.c; Y[j] = cc.mad_hi_cc(a[lane][j], b, Y[j + 2], c)
+        c = cc.c; Y[L - 2] = cc.mad_lo_cc(a[lane][L - 1], b, 0, c)
+        c = cc.c; Y[L - 1] = cc.mad_hi_cc(a[lane][L - 1], b, hi, c)
+        hi = cc.c
+        X[0] = cc.mad_lo_cc(a[lane][0], b, X[0])
+        c = cc.c; X[1] = cc.mad_hi_cc(a[lane][0], b, X[1], c)
+        for j in range(2, L, 2):
+            c = cc.c; X[j] = cc.mad_lo_cc(a[lane][j], b, X[j], c)
+            c = cc.c; X[j + 1] = cc.mad_hi_cc(a[lane][j], b, X[j + 1], c)
+        c = cc.c; Y[L - 1] = cc.add_cc(Y[L - 1], 0, c)
+        hi = hi + cc.c
+        st[lane] = (X, Y, hi)
+        ms.append((X[0] * n0inv) & M32)
+    m = ms[0]
+    for lane in (0, 1):
+        X, Y, hi = st[lane]
+        nn = n[lane]
+        cc = CC()
+        Y[0] = cc.mad_lo_cc(nn[1], m, Y[0])
+        c = cc.c; Y[1] = cc.mad_hi_cc(nn[1], m, Y[1], c)
+        for j in range(3, L, 2):
+            c = cc.c; Y[j - 1] = cc.mad_lo_cc(nn[j], m, Y[j - 1], c)
+            c = cc.c; Y[j] = cc.mad_hi_cc(nn[j], m, Y[j], c)
+        hi = hi + cc.c
+        X[0] = cc.mad_lo_cc(nn[0], m, X[0])
+        c = cc.c; X[1] = cc.mad_hi_cc(nn[0], m, X[1], c)
+        for j in range(2, L, 2):
+            c = cc.c; X[j] = cc.mad_lo_cc(nn[j], m, X[j], c)
+            c = cc.c; X[j + 1] = cc.mad_hi_cc(nn[j], m, X[j + 1], c)
+        c = cc.c; Y[L - 1] = cc.add_cc(Y[L - 1], 0, c)
+        hi = hi + cc.c
+        st[lane] = (X, Y, hi)
+    assert st[0][0][0] == 0
+    w = [st[1][0][0], st[0][0][0]]          # shfl_xor(X[0], 1)
+    for lane in (0, 1):
+        X, Y, hi = st[lane]
+        cc = CC()
+        Y[L - 1] = cc.add_cc(Y[L - 1], w[lane])  # new even array's top, carry -> hi
+        hi = hi + cc.c
+        assert hi < 2**32
+        st[lane] = (Y, X, hi)                  # role swap
+
+
+def montmul_pair_model(A, B, N, L):
+    S = 2 * L
+    n0inv = (-pow(N & M32, -1, 2**32)) % 2**32
+    a = [L_(A, 0, L), L_(A, L, L)]
+    n = [L_(N, 0, L), L_(N, L, L)]
+    st = [([0] * L, [0] * L, 0), ([0] * L, [0] * L, 0)]
+    for i in range(S):
+        cios_step_pair(st, a, (B >> (32 * i)) & M32, n, n0inv, L)
+    vals = []
+    for lane in (0, 1):
+        X, Y, hi = st[lane]
+        r = X[0] + Y[1] + sum((X[k] + Y[k + 1]) << (32 * k) for k in range(1, L - 1)) \
+            + (X[L - 1] << (32 * (L - 1))) + (hi << (32 * L))
+        vals.append(r)
+    T = vals[0] + (vals[1] << (32 * L))
+    return T - N if T >= N else T
+
+
+def L_(x, off, L):
+    return [(x >> (32 * (off + k))) & M32 for k in range(L)]
+
+
+@pytest.mark.parametrize("L", [2, 4, 8])
+def test_cios_pair_model(L):
+    rnd = random.Random(100 + L)
+    S = 2 * L
+    R = 1 << (32 * S)
+    cases = [(R - 1, R - 1, R - 2), (R - 3, R - 4, 1)]
+    for _ in range(200):
+        N = rnd.getrandbits(32 * S) | 1 | (rnd.choice([1, 0]) << (32 * S - 1))
+        cases.append((N, rnd.randrange(R), rnd.randrange(N)))
+    for N, A, B in cases:
+        if N < 3:
+            continue
+        B %= N
+        got = montmul_pair_model(A, B, N, L)
+        assert got == (A * B * pow(R, -1, N)) % N

@@ -92,7 +92,7 @@ def test_fig4_worked_example(R):
 # ------------------------------------------------------------------ multi-precision widths
 
 WIDTHS = ["rsa64", "rsa96", "rsa128", "rsa192", "rsa256", "rsa384", "rsa512", "rsa768", "rsa1000",
-          "rsa1024", "rsa1536", "rsa2048"]
+          "rsa1024", "rsa1536", "rsa2048", "rsa3072", "rsa4096"]
 
 
 @pytest.mark.parametrize("key", WIDTHS)
@@ -112,7 +112,7 @@ def test_parity_private_exponent(R, key):
     k = workload.key(key)
     nb, n = k["nbits"], k["n"]
     s = workload.limbs_needed(nb)
-    count = 40000 + 11 if nb <= 128 else (4096 + 9 if nb <= 512 else 600 + 3)
+    count = 40000 + 11 if nb <= 128 else (4096 + 9 if nb <= 512 else (600 + 3 if nb <= 2048 else 160 + 3))
     base = workload.packets(count, nb, n=n, config_id=3)
     got = gpu_run(R, base, k["d"], n, nb)
     assert np.array_equal(got, oracle_rows(base, k["d"], n, s))
@@ -134,7 +134,7 @@ def test_forced_windows_agree(R, w):
 
 # ------------------------------------------------------------------ edge cases
 
-@pytest.mark.parametrize("key", ["rsa64", "rsa1000", "rsa2048"])
+@pytest.mark.parametrize("key", ["rsa64", "rsa1000", "rsa2048", "rsa3072", "rsa4096"])
 def test_edge_exponents_and_bases(R, key):
     k = workload.key(key)
     nb, n = k["nbits"], k["n"]
@@ -174,9 +174,9 @@ def test_argument_errors(R):
     with pytest.raises(R.RsaError) as ei:
         R.rsa_modexp_batch(torch.zeros((4, 1), dtype=torch.int32, device="cuda"), 3, 1, 1)
     assert ei.value.code == R.RSA_ERANGE
-    big = torch.zeros((4, 128), dtype=torch.int32, device="cuda")
+    big = torch.zeros((4, 129), dtype=torch.int32, device="cuda")
     with pytest.raises(R.RsaError) as ei:
-        R.rsa_modexp_batch(big, 3, (1 << 4095) + 1, 4096)
+        R.rsa_modexp_batch(big, 3, (1 << 4096) + 1, 4097)
     assert ei.value.code == R.RSA_ERANGE
 
 
@@ -244,3 +244,19 @@ def test_full_size_u64(R):
     idx = _sample(len(m), 20000)
     assert np.array_equal(c[idx], oracle_rows(m[idx], k["e"], k["n"], 2))
     assert np.array_equal(y[idx], oracle_rows(c[idx], k["d"], k["n"], 2))
+
+
+def test_full_size_rsa4096_decrypt(R):
+    """C4: 256K packets, full 4095-bit d (lane-pair kernel): y == m on every
+    packet for oracle ciphertexts of a sample, oracle parity on a subsample,
+    and the GPU round trip on the whole batch."""
+    k = workload.key("rsa4096")
+    cfg = workload.CONFIGS["rsa4096-dec"]
+    m = workload.packets(cfg["count"], 4096, n=k["n"], config_id=cfg["config_id"])
+    c_gpu = gpu_run(R, m, k["e"], k["n"], 4096)
+    idx = _sample(len(m), 3000)
+    assert np.array_equal(c_gpu[idx], oracle_rows(m[idx], k["e"], k["n"], 128))
+    y = gpu_run(R, c_gpu, k["d"], k["n"], 4096)
+    assert np.array_equal(y, m)
+    sub = idx[:40]
+    assert np.array_equal(y[sub], oracle_rows(c_gpu[sub], k["d"], k["n"], 128))

@@ -38,7 +38,7 @@ def main():
         print(f"== {name}  ({len(ins)} instructions)")
         loops = []
         for a, t in ins:
-            m = re.search(r"BRA\s+(?:\S+\s+)?0x([0-9a-f]+)", t)
+            m = re.search(r"BRA(?:\.\w+)?\s+(?:\S+\s+)?0x([0-9a-f]+)", t)
             if m and int(m.group(1), 16) < a:
                 lo = int(m.group(1), 16)
                 body = [x for x in ins if lo <= x[0] <= a]
