@@ -287,16 +287,18 @@ def run_ours(args, rank, world, local_rank):
     f_max = float(peaks.get("sm_max_mhz", 1965.0))
     dom = max(range(len(legs)), key=lambda j: leg_ms[j])
     S = plans[dom]["width_class"]
-    prod_per_mm = 2 * S * S + S
-    products = count * plans[dom]["montmuls"] * prod_per_mm
+    products = count * plans[dom]["products"]
     achieved = products / (leg_ms[dom] / 1e3) / 1e12
     peak = R_PRODUCTS_PER_CLK_PER_SM * sms * f_max * 1e6 / 1e12
     roofline = {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "Tprod/s", "frac": achieved / peak,
                 "traffic": ncu_traffic(key_name, legs[dom][0], count),
                 "traffic_unit": "bytes per launch", "algorithmic_bytes": count * s * 4 * 2,
                 "kernel": (f"modexp_pair_kernel<{S}>" if S == 128 else f"modexp_kernel<{S}>") + f" ({legs[dom][0]})",
-                "algorithmic": f"{plans[dom]['montmuls']} montmul/packet x (2S^2+S = {prod_per_mm}) 32x32->64 "
-                               f"limb products x {count} packets per launch",
+                "algorithmic": f"{plans[dom]['products']} 32x32->64 limb products/packet "
+                               f"({plans[dom]['squarings']} squarings x "
+                               f"{'1.5S^2+1.5S' if plans[dom]['sqr_kernel'] else '2S^2+S'} + "
+                               f"{plans[dom]['montmuls'] - plans[dom]['squarings']} other montmuls x 2S^2+S, S={S})"
+                               f" x {count} packets per launch",
                 "peak_basis": f"{R_PRODUCTS_PER_CLK_PER_SM} products/clk/SM (IMAD.WIDE half rate, "
                               f"profiles/r01_imad_peak.jsonl) x {sms} SMs x {f_max:.0f} MHz "
                               f"(MEASURED_PEAKS sm_max_mhz)"}
@@ -305,7 +307,8 @@ def run_ours(args, rank, world, local_rank):
     legs_out = {}
     for j, (label, field) in enumerate(legs):
         legs_out[label] = {"ms": leg_ms[j], "modexp_per_s": world * count / (leg_ms[j] / 1e3),
-                           "montmuls_per_packet": plans[j]["montmuls"], "window": plans[j]["window"],
+                           "montmuls_per_packet": plans[j]["montmuls"], "squarings_per_packet": plans[j]["squarings"],
+                           "products_per_packet": plans[j]["products"], "window": plans[j]["window"],
                            "exp_bits": plans[j]["exp_bits"]}
     cpu = None
     if not args.no_cpu_baseline and world == 1:

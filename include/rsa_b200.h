@@ -112,6 +112,9 @@ typedef struct {
     int exp_bits;         /* bit length of exp */
     int grid;             /* persistent grid (CTAs) */
     int block;            /* threads per CTA */
+    int sqr_kernel;       /* 1 if squarings use the dedicated squaring (1.5S^2+1.5S products) */
+    long long products;   /* algorithmic 32x32->64 limb products per packet: squarings x
+                             (1.5S^2+1.5S or 2S^2+S) + other montmuls x (2S^2+S) */
 } rsa_plan_info_t;
 
 int rsa_plan_info(const uint32_t* exp, const uint32_t* n, int nbits, rsa_plan_info_t* info);

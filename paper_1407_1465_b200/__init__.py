@@ -44,7 +44,7 @@ class RsaPlanInfo(ctypes.Structure):
     _fields_ = [("width_class", ctypes.c_int), ("s_io", ctypes.c_int), ("window", ctypes.c_int),
                 ("table_entries", ctypes.c_int), ("nops", ctypes.c_int), ("montmuls", ctypes.c_longlong),
                 ("squarings", ctypes.c_longlong), ("exp_bits", ctypes.c_int), ("grid", ctypes.c_int),
-                ("block", ctypes.c_int)]
+                ("block", ctypes.c_int), ("sqr_kernel", ctypes.c_int), ("products", ctypes.c_longlong)]
 
 
 _lib.rsa_strerror.restype = ctypes.c_char_p

@@ -18,14 +18,19 @@
 
 #include "mont.cuh"
 #include "mont_pair.cuh"
+#include "mont_sqr.cuh"
 #include "plan.h"
 
 namespace rsa_b200 {
 
 template <int S>
 struct KCfg {
-    static constexpr int BLOCK = 128;
-    static constexpr int MINB = (S >= 64) ? 2 : (S >= 32 ? 3 : 4);
+    // S = 64: one 256-thread CTA per SM and a barrier per Montgomery op keep all
+    // 8 warps of an SM on the same code lines (the squaring + multiply code is
+    // larger than the instruction cache; drifting warps thrash it).
+    static constexpr int BLOCK = (S >= 64) ? 256 : 128;
+    static constexpr int MINB = (S >= 64) ? 1 : (S >= 32 ? 3 : 4);
+    static constexpr bool LOCKSTEP = (S >= 32);
 };
 
 template <int S>
@@ -41,7 +46,13 @@ modexp_kernel(const __grid_constant__ ModexpParams<S> p) {
     const unsigned nthr = gridDim.x * blockDim.x;
     V* const table = reinterpret_cast<V*>(p.table);
 
-    for (unsigned long long pkt = gtid; pkt < p.count; pkt += nthr) {
+    // every thread runs the same number of trips (uniform barriers); an
+    // out-of-range trip recomputes the last packet and skips the store
+    const unsigned long long trips = (p.count + nthr - 1) / nthr;
+    for (unsigned long long t = 0; t < trips; t++) {
+        const unsigned long long pkt0 = gtid + t * nthr;
+        const bool valid = pkt0 < p.count;
+        const unsigned long long pkt = valid ? pkt0 : p.count - 1;
         uint32_t a[S];
         // a2: load the packet (packet-major at the boundary), zero padded
         const uint32_t* src = p.base + pkt * (unsigned long long)p.s_io;
@@ -67,15 +78,13 @@ modexp_kernel(const __grid_constant__ ModexpParams<S> p) {
                 }
             }
             for (int r = 0; r < op.rep; r++) {
-                // stage the b operand in this thread's shared-memory slot
+                if constexpr (KCfg<S>::LOCKSTEP) __syncthreads();
                 if (op.kind == RSA_OP_SQR) {
-#pragma unroll
-                    for (int g = 0; g < NG; g++) {
-                        V v; v.x = a[G * g]; v.y = a[G * g + 1];
-                        if constexpr (G == 4) { v.z = a[G * g + 2]; v.w = a[G * g + 3]; }
-                        bslot[g * stride] = v;
-                    }
-                } else if (op.kind == RSA_OP_MUL) {
+                    montsqr<S>(a, p.n, p.n0inv);      // 1.5 S^2 + 1.5 S products
+                    continue;
+                }
+                // stage the b operand in this thread's shared-memory slot
+                if (op.kind == RSA_OP_MUL) {
 #pragma unroll
                     for (int g = 0; g < NG; g++)
                         bslot[g * stride] = table[((size_t)op.bidx * NG + g) * nthr + gtid];
@@ -107,15 +116,17 @@ modexp_kernel(const __grid_constant__ ModexpParams<S> p) {
         }
 
         // a8: store the canonical result
-        uint32_t* dst = p.out + pkt * (unsigned long long)p.s_io;
-        if (p.s_io == S && (S % 4) == 0) {
+        if (valid) {
+            uint32_t* dst = p.out + pkt * (unsigned long long)p.s_io;
+            if (p.s_io == S && (S % 4) == 0) {
 #pragma unroll
-            for (int k = 0; k < S; k += 4)
-                *reinterpret_cast<uint4*>(dst + k) = make_uint4(a[k], a[k + 1], a[k + 2], a[k + 3]);
-        } else {
+                for (int k = 0; k < S; k += 4)
+                    *reinterpret_cast<uint4*>(dst + k) = make_uint4(a[k], a[k + 1], a[k + 2], a[k + 3]);
+            } else {
 #pragma unroll
-            for (int k = 0; k < S; k++)
-                if (k < p.s_io) dst[k] = a[k];
+                for (int k = 0; k < S; k++)
+                    if (k < p.s_io) dst[k] = a[k];
+            }
         }
     }
 }

@@ -203,8 +203,13 @@ static int get_plan(const uint32_t* exp, const uint32_t* n, int nbits, Plan* out
             int ntab;
             long long mm, sq;
             if (!build_ops(E, w, &ops, &ntab, &mm, &sq)) continue;
-            if (best < 0 || mm < best) {
-                best = mm;
+            // minimise executed limb products (squarings are cheaper when the
+            // dedicated squaring kernel is used, S <= 64)
+            const long long S = pl.S;
+            const long long sqc = (pl.S <= 64) ? (3 * S * S + 3 * S) / 2 : 2 * S * S + S;
+            const long long cost = sq * sqc + (mm - sq) * (2 * S * S + S);
+            if (best < 0 || cost < best) {
+                best = cost;
                 best_ops = ops;
                 pl.window = w;
                 pl.ntab = ntab;
@@ -399,6 +404,10 @@ int rsa_plan_info(const uint32_t* exp, const uint32_t* n, int nbits, rsa_plan_in
     info->montmuls = pl.montmuls;
     info->squarings = pl.squarings;
     info->exp_bits = pl.exp_bits;
+    const long long S = pl.S;
+    info->sqr_kernel = (pl.S <= 64) ? 1 : 0;     // modexp.cu: montsqr for S <= 64
+    const long long sq_cost = info->sqr_kernel ? (3 * S * S + 3 * S) / 2 : 2 * S * S + S;
+    info->products = pl.squarings * sq_cost + (pl.montmuls - pl.squarings) * (2 * S * S + S);
     const int sms = device_sms();
     if (sms) {
         size_t nthr;

@@ -206,3 +206,105 @@ def test_cios_pair_model(L):
         B %= N
         got = montmul_pair_model(A, B, N, L)
         assert got == (A * B * pow(R, -1, N)) % N
+
+
+# ---------------------------------------------------------------- squaring (mont_sqr.cuh)
+
+def red_step(X, Y, hi, n, n0inv):
+    S = len(X)
+    cc = CC()
+    X[0] = cc.add_cc(X[0], Y[1])
+    m = (X[0] * n0inv) & M32
+    for j in range(1, S - 2, 2):
+        c = cc.c; Y[j - 1] = cc.mad_lo_cc(n[j], m, Y[j + 1], c)
+        c = cc.c; Y[j] = cc.mad_hi_cc(n[j], m, Y[j + 2], c)
+    c = cc.c; Y[S - 2] = cc.mad_lo_cc(n[S - 1], m, 0, c)
+    c = cc.c; Y[S - 1] = cc.mad_hi_cc(n[S - 1], m, hi, c)
+    hi = cc.c
+    X[0] = cc.mad_lo_cc(n[0], m, X[0])
+    assert X[0] == 0
+    c = cc.c; X[1] = cc.mad_hi_cc(n[0], m, X[1], c)
+    for j in range(2, S, 2):
+        c = cc.c; X[j] = cc.mad_lo_cc(n[j], m, X[j], c)
+        c = cc.c; X[j + 1] = cc.mad_hi_cc(n[j], m, X[j + 1], c)
+    c = cc.c; Y[S - 1] = cc.add_cc(Y[S - 1], 0, c)
+    hi = hi + cc.c
+    return hi
+
+
+def montsqr_model(a, n, S):
+    n0inv = (-pow(n[0], -1, 2**32)) % 2**32
+    # phase 1: triangle by product scanning, two accumulators per column
+    T = [0] * (2 * S)
+    c0 = c1 = c2 = 0
+    for k in range(1, 2 * S - 2):
+        lo, hi_ = max(0, k - S + 1), (k - 1) // 2
+        d0 = d1 = d2 = 0
+        for i in range(lo, hi_ + 1):
+            p = a[i] * a[k - i]
+            if (i - lo) % 2 == 0:
+                s = c0 + (c1 << 32) + p
+                c0, c1 = s & M32, (s >> 32) & M32
+                c2 += s >> 64
+            else:
+                s = d0 + (d1 << 32) + p
+                d0, d1 = s & M32, (s >> 32) & M32
+                d2 += s >> 64
+        cc = CC()
+        c0 = cc.add_cc(c0, d0)
+        c = cc.c; c1 = cc.add_cc(c1, d1, c)
+        c2 = (c2 + d2 + cc.c) & M32
+        T[k] = c0
+        c0, c1, c2 = c1, c2, 0
+    T[2 * S - 2] = c0
+    T[2 * S - 1] = c1
+    # phase 2: double;  phase 3: + diagonal
+    cc = CC()
+    T[0] = cc.add_cc(T[0], T[0])
+    for k in range(1, 2 * S):
+        c = cc.c; T[k] = cc.add_cc(T[k], T[k], c)
+    assert cc.c == 0
+    cc = CC()
+    for i in range(S):
+        c = cc.c if i else 0
+        T[2 * i] = cc.mad_lo_cc(a[i], a[i], T[2 * i], c)
+        c = cc.c; T[2 * i + 1] = cc.mad_hi_cc(a[i], a[i], T[2 * i + 1], c)
+    assert cc.c == 0
+    A = sum(v << (32 * k) for k, v in enumerate(a))
+    assert sum(v << (32 * k) for k, v in enumerate(T)) == A * A
+    # phase 4: reduce T_low
+    X, Y, hi = T[:S], [0] * S, 0
+    for i in range(S):
+        hi = red_step(X, Y, hi, n, n0inv) if i % 2 == 0 else red_step(Y, X, hi, n, n0inv)
+    cc = CC()
+    X[0] = cc.add_cc(X[0], Y[1])
+    for k in range(1, S - 1):
+        c = cc.c; X[k] = cc.add_cc(X[k], Y[k + 1], c)
+    c = cc.c; X[S - 1] = cc.add_cc(X[S - 1], 0, c)
+    hi = hi + cc.c
+    # + T_high
+    cc = CC()
+    for k in range(S):
+        c = cc.c if k else 0
+        X[k] = cc.add_cc(X[k], T[S + k], c)
+    hi = hi + cc.c
+    r = sum(v << (32 * k) for k, v in enumerate(X)) + (hi << (32 * S))
+    N = sum(v << (32 * k) for k, v in enumerate(n))
+    assert r < 2 * N
+    return r - N if r >= N else r
+
+
+@pytest.mark.parametrize("S", [2, 4, 8, 16])
+def test_montsqr_model(S):
+    rnd = random.Random(200 + S)
+    R = 1 << (32 * S)
+    cases = []
+    for N in [R - 1, R - 3, (R >> 1) | 1]:
+        cases += [(N, N - 1), (N, 0), (N, 1), (N, N // 2)]
+    for _ in range(200):
+        N = rnd.getrandbits(32 * S) | 1 | (rnd.choice([1, 0]) << (32 * S - 1))
+        if N >= 3:
+            cases.append((N, rnd.randrange(N)))
+    for N, A in cases:
+        got = montsqr_model(L(A, S), L(N, S), S)
+        assert got == (A * A * pow(R, -1, N)) % N
