@@ -54,7 +54,7 @@ def parse():
     ap.add_argument("--count", type=int, default=0, help="override packets per rank (profiling only)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--cpu-seconds", type=float, default=15.0, help="CPU-seconds budget of the oracle sample")
+    ap.add_argument("--cpu-seconds", type=float, default=20.0, help="CPU-seconds budget of the oracle sample")
     return ap.parse_args()
 
 

@@ -349,11 +349,22 @@ int rsa_modexp_batch_host(const uint32_t* base_host, const uint32_t* exp, const 
     if (st) return st;
     const int s = (nbits + 31) / 32;
     const size_t row = (size_t)s * sizeof(uint32_t);
-    // chunking: up to 8 chunks of >= 64K packets, two streams ping-pong
-    size_t nch = count / 65536;
+    // chunking: up to 8 chunks, two streams ping-pong (copies of one chunk
+    // overlap the kernel of the other); each chunk is a whole number of
+    // persistent-grid waves so no chunk ends in a partly idle wave
+    size_t wave = 1;
+    {
+        const int sms = device_sms();
+        int grid = 0, block = 0;
+        size_t slots = 0;
+        if (sms && !pl.exp_zero && rsa_b200_grid(pl.S, sms, &grid, &block, &slots) == cudaSuccess && slots)
+            wave = slots;
+    }
+    const size_t waves = (count + wave - 1) / wave;
+    size_t nch = waves < 8 ? waves : 8;
     if (nch < 1) nch = 1;
-    if (nch > 8) nch = 8;
-    const size_t per = (count + nch - 1) / nch;
+    const size_t per = ((waves + nch - 1) / nch) * wave;
+    nch = (count + per - 1) / per;
     cudaStream_t ss[2];
     if (cudaStreamCreateWithFlags(&ss[0], cudaStreamNonBlocking) != cudaSuccess) return RSA_ECUDA;
     if (cudaStreamCreateWithFlags(&ss[1], cudaStreamNonBlocking) != cudaSuccess) {
