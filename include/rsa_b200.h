@@ -99,6 +99,19 @@ int rsa_modexp_batch(const uint32_t* base, const uint32_t* exp, const uint32_t* 
 int rsa_modexp_batch_host(const uint32_t* base_host, const uint32_t* exp, const uint32_t* n,
                           int nbits, size_t count, uint32_t* out_host);
 
+/* The paper's own GPU kernel, for comparison:
+ * Alg 1 / Fig 11 + Alg 2 / Fig 12, one thread
+ * per packet, 64 threads per block, O(key) loop: result[i] = num[i]^key mod
+ * den computed as floor(key/2) multiplications by (num mod den)^2 and one by
+ * (num mod den) if key is odd.  Exact integers (see modexp.cu).
+ *   num, result : DEVICE pointers, `count` uint32 values each.
+ *   key < 2^32, 1 <= den < 2^31 (the kernel's single-word envelope);
+ *   faithful != 0 keeps the paper's key == 0 -> num mod den,
+ *   faithful == 0 returns 1 mod den.  Asynchronous on `stream`.
+ * Errors: RSA_ERANGE (den or key out of range), RSA_EINVAL, RSA_ECUDA. */
+int rsa_modexp_batch_paper(const uint32_t* num, uint64_t key, uint32_t den, size_t count,
+                           uint32_t* result, int faithful, void* stream);
+
 /* Plan summary for (exp, n, nbits): the width class, window and the number
  * of Montgomery multiplications each packet costs (for the roofline). */
 typedef struct {

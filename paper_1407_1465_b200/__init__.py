@@ -30,7 +30,7 @@ RSA_MAX_NBITS = 4096
 
 EXPORTS = ["rsa_strerror", "rsa_keygen_check", "rsa_validate_key", "rsa_modexp_batch",
            "rsa_modexp_batch_host", "rsa_plan_info", "rsa_set_window", "rsa_encode", "rsa_decode",
-           "rsa_kernel_launches"]
+           "rsa_kernel_launches", "rsa_modexp_batch_paper"]
 
 if not os.path.exists(LIB_PATH):
     raise ImportError(f"{LIB_PATH} is not built: run `python -m paper_1407_1465_b200.build` "
@@ -60,6 +60,8 @@ _lib.rsa_set_window.argtypes = [ctypes.c_int]
 _lib.rsa_encode.argtypes = [ctypes.c_char_p, _u32p, ctypes.c_size_t, ctypes.POINTER(ctypes.c_size_t)]
 _lib.rsa_decode.argtypes = [_u32p, ctypes.c_size_t, ctypes.c_char_p, ctypes.c_size_t]
 _lib.rsa_kernel_launches.restype = ctypes.c_ulonglong
+_lib.rsa_modexp_batch_paper.argtypes = [ctypes.c_void_p, ctypes.c_uint64, ctypes.c_uint32, ctypes.c_size_t,
+                                        ctypes.c_void_p, ctypes.c_int, ctypes.c_void_p]
 
 
 class RsaError(RuntimeError):
@@ -135,6 +137,24 @@ def rsa_modexp_batch_host(base: np.ndarray, exp: int, n: int, nbits: int, out: n
     op = out.ctypes.data if isinstance(out, np.ndarray) else out.data_ptr()
     rc = _lib.rsa_modexp_batch_host(ctypes.c_void_p(bp), _p(E), _p(N), nbits, base.shape[0], ctypes.c_void_p(op))
     _check(rc, "rsa_modexp_batch_host")
+    return out
+
+
+def rsa_modexp_batch_paper(num, key: int, den: int, faithful: bool = True, out=None, stream=None):
+    """The paper's Fig 12 kernel on the GPU (prior art): num is a CUDA
+    int32/uint32 tensor of single-word packets; returns result tensor."""
+    import torch
+    num = num.contiguous().view(-1)
+    if out is None:
+        out = torch.empty_like(num)
+    if stream is None:
+        stream = torch.cuda.current_stream(num.device).cuda_stream
+    elif hasattr(stream, "cuda_stream"):
+        stream = stream.cuda_stream
+    with torch.cuda.device(num.device):
+        rc = _lib.rsa_modexp_batch_paper(ctypes.c_void_p(num.data_ptr()), key, den, num.numel(),
+                                         ctypes.c_void_p(out.data_ptr()), 1 if faithful else 0, ctypes.c_void_p(stream))
+    _check(rc, "rsa_modexp_batch_paper")
     return out
 
 

@@ -259,6 +259,38 @@ static cudaError_t launch_pair(const void* params, int sms, cudaStream_t stream,
     return cudaGetLastError();
 }
 
+
+// ---------------------------------------------------------------------------
+// The paper's own kernel: Alg 1 / Fig 11
+// with the device function of Alg 2 / Fig 12
+// (PAPER.md:252-294, 374-406), as prior art beside the Montgomery path.  One
+// thread per packet; a = (g % n)^2 unreduced; floor(e/2) times
+// ret = (ret * a) % n, then ret = (ret * (g % n)) % n if e is odd.  Exact
+// integer form of the float counter (reading Z15); `faithful` keeps the
+// paper's e == 0 -> g % n (reading Z5), else 1 % n.  Moduli < 2^31 (checked
+// on the host).  Exact integers: a = g^2 < 2^62 is kept in 64 bits and
+// reduced before each product (ret * (a % n) < 2^62), i.e. the mathematical
+// meaning of Fig 12 -- the paper's 32-bit `unsigned int a` wraps for
+// g > 65535; the oracle's halving() follows the same reading.
+// The write is a plain store: Fig 11's atomicExch is unnecessary (disjoint).
+__global__ void paper_fig12_kernel(const uint32_t* __restrict__ num, uint64_t key, uint32_t den,
+                                   unsigned long long count, int faithful, uint32_t* __restrict__ result) {
+    const unsigned long long i = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x;   // Alg 1 step 3
+    if (i >= count) return;                                                                  // Alg 1 step 4
+    const uint64_t g = num[i] % den;
+    uint64_t ret;
+    if (key == 0) {
+        ret = faithful ? g : (1u % den);
+    } else {
+        const uint64_t a = g * g;                          // "(base%den)*(base%den)", unreduced
+        ret = 1;
+        for (uint64_t h = key / 2; h > 0; h--) ret = (ret * (a % den)) % den;   // size > 0.5 branch
+        if (key & 1) ret = (ret * g) % den;                                      // size == 0.5 branch
+        ret %= den;
+    }
+    result[i] = (uint32_t)ret;
+}
+
 // exp == 0: every output is 1 mod n = 1 (n >= 3), reading Z12
 __global__ void fill_one_kernel(uint32_t* out, unsigned long long count, int s_io) {
     const unsigned long long total = count * (unsigned long long)s_io;
@@ -341,5 +373,14 @@ size_t rsa_b200_params_size(int S) {
 cudaError_t rsa_b200_fill_one(uint32_t* out, unsigned long long count, int s_io, int sms, cudaStream_t stream) {
     if (count == 0) return cudaSuccess;
     rsa_b200::fill_one_kernel<<<sms * 4, 256, 0, stream>>>(out, count, s_io);
+    return cudaGetLastError();
+}
+
+cudaError_t rsa_b200_paper_fig12(const uint32_t* num, uint64_t key, uint32_t den, unsigned long long count,
+                                 int faithful, uint32_t* result, cudaStream_t stream) {
+    if (count == 0) return cudaSuccess;
+    const int block = 64;   // the paper's Table 1 shape (64 threads per block)
+    const unsigned long long grid = (count + block - 1) / block;
+    rsa_b200::paper_fig12_kernel<<<(unsigned)grid, block, 0, stream>>>(num, key, den, count, faithful, result);
     return cudaGetLastError();
 }

@@ -24,6 +24,8 @@ cudaError_t rsa_b200_launch(int S, const void* params, int sms, cudaStream_t str
 cudaError_t rsa_b200_grid(int S, int sms, int* grid, int* block, size_t* nthreads);
 size_t rsa_b200_params_size(int S);
 cudaError_t rsa_b200_fill_one(uint32_t* out, unsigned long long count, int s_io, int sms, cudaStream_t stream);
+cudaError_t rsa_b200_paper_fig12(const uint32_t* num, uint64_t key, uint32_t den, unsigned long long count,
+                                 int faithful, uint32_t* result, cudaStream_t stream);
 
 using rsa_host::BN;
 
@@ -424,6 +426,18 @@ int rsa_plan_info(const uint32_t* exp, const uint32_t* n, int nbits, rsa_plan_in
         size_t nthr;
         rsa_b200_grid(pl.S, sms, &info->grid, &info->block, &nthr);
     }
+    return RSA_OK;
+}
+
+int rsa_modexp_batch_paper(const uint32_t* num, uint64_t key, uint32_t den, size_t count, uint32_t* result,
+                           int faithful, void* stream) {
+    if (den == 0 || den >= (1u << 31)) return RSA_ERANGE;
+    if (key >= (1ull << 32)) return RSA_ERANGE;
+    if (count == 0) return RSA_OK;
+    if (!num || !result) return RSA_EINVAL;
+    if (rsa_b200_paper_fig12(num, key, den, count, faithful ? 1 : 0, result, (cudaStream_t)stream) != cudaSuccess)
+        return RSA_ECUDA;
+    g_launches++;
     return RSA_OK;
 }
 

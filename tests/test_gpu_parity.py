@@ -260,3 +260,43 @@ def test_full_size_rsa4096_decrypt(R):
     assert np.array_equal(y, m)
     sub = idx[:40]
     assert np.array_equal(y[sub], oracle_rows(c_gpu[sub], k["d"], k["n"], 128))
+
+
+# ------------------------------------------------------------------ f2: the paper's Fig 12 kernel
+
+@pytest.mark.parametrize("key", ["toy17947", "table2_513581", "fig2_187"])
+def test_paper_fig12_kernel_matches_oracle(R, key):
+    k = workload.key(key)
+    n, e = k["n"], k["e"]
+    base = np.arange(min(n, 65536), dtype=np.uint32)
+    t = torch.from_numpy(base.view(np.int32)).cuda()
+    for exp in (e, 0, 1, 2, 1000):
+        for faithful in (True, False):
+            got = R.rsa_modexp_batch_paper(t, exp, n, faithful=faithful)
+            torch.cuda.synchronize()
+            got = got.cpu().numpy().view(np.uint32)
+            want = np.array([oracle.halving(int(g), exp, n, faithful) for g in base[:3000]], dtype=np.uint32)
+            assert np.array_equal(got[:3000], want), (exp, faithful)
+            if exp or not faithful:
+                assert np.array_equal(got, oracle_rows(base.reshape(-1, 1), exp, n, 1).ravel())
+
+
+def test_paper_fig12_table1_shapes(R):
+    """Table 1 shapes: n = 131*137, e = 131, paper inputs
+    0..800, sizes 256 .. 32784; both kernels agree with the oracle."""
+    n, e = 17947, 131
+    for size in (256, 512, 1024, 2048, 4096, 8192, 16392, 32784):
+        pp = workload.paper_packets(size, config_id=size)
+        t = torch.from_numpy(pp.ravel().view(np.int32)).cuda()
+        got = R.rsa_modexp_batch_paper(t, e, n).cpu().numpy().view(np.uint32)
+        mont = gpu_run(R, pp, e, n, 15).ravel()
+        want = oracle_rows(pp, e, n, 1).ravel()
+        assert np.array_equal(got, want) and np.array_equal(mont, want)
+
+
+def test_paper_fig12_errors(R):
+    t = torch.zeros(4, dtype=torch.int32, device="cuda")
+    for den, key in [(0, 3), (1 << 31, 3), (17947, 1 << 32)]:
+        with pytest.raises(R.RsaError) as ei:
+            R.rsa_modexp_batch_paper(t, key, den)
+        assert ei.value.code == R.RSA_ERANGE
