@@ -112,6 +112,51 @@ int rsa_modexp_batch_host(const uint32_t* base_host, const uint32_t* exp, const 
 int rsa_modexp_batch_paper(const uint32_t* num, uint64_t key, uint32_t den, size_t count,
                            uint32_t* result, int faithful, void* stream);
 
+/* ---- multi-key batches and GPU prime search ----
+ * rsa_modexp_batch_multi: out[i] = base[i]^exps[i] mod mods[i], every packet
+ * with its own exponent and modulus (e.g. encrypting to many recipients).
+ *   base, exps, mods, out: DEVICE, [count][s] limbs, s = ceil(nbits/32),
+ *   2 <= nbits <= 2048; exps are scanned over their low exp_bits bits
+ *   (1 <= exp_bits <= 32 s) with a fixed window; every mods[i] must be odd and
+ *   >= 3 -- packets whose modulus is not get out = 0 and, if `status` (DEVICE,
+ *   count int32, may be NULL) is given, status[i] = RSA_EEVEN (else 0).
+ *   n', R mod n and R^2 mod n are derived per packet on the device.
+ *   Asynchronous on `stream`.  Errors: RSA_ERANGE, RSA_EINVAL, RSA_ECUDA. */
+int rsa_modexp_batch_multi(const uint32_t* base, const uint32_t* exps, const uint32_t* mods, int nbits,
+                           int exp_bits, size_t count, uint32_t* out, int32_t* status, void* stream);
+
+/* One Miller-Rabin round to base `base` (>= 2) on every candidate (DEVICE,
+ * [count][s], odd, > base): verdict[i] (DEVICE, uint32) = 1 if cand[i] is a
+ * strong probable prime to that base, else 0.  4 <= nbits <= 2048.  Async. */
+int rsa_miller_rabin_batch(const uint32_t* cand, int nbits, size_t count, uint32_t base, uint32_t* verdict,
+                           void* stream);
+
+/* The prime search's candidate generator (counter based, reproducible):
+ * candidate `first + i` -> out[i] (DEVICE, [count][s]); exactly nbits bits
+ * with the top two bits and bit 0 set.  Async. */
+int rsa_prime_candidates(int nbits, uint64_t seed, unsigned long long first, size_t count, uint32_t* out,
+                         void* stream);
+
+/* Small-prime sieve: verdict[i] = 0 if cand[i] has a prime factor < 4096
+ * other than itself, else 1 (DEVICE arrays).  Async. */
+int rsa_prime_sieve(const uint32_t* cand, int nbits, size_t count, uint32_t* verdict, void* stream);
+
+/* Find `want` primes of nbits bits (16 <= nbits <= 2048): generator + sieve +
+ * `rounds` (1..16) Miller-Rabin rounds, bases 2, 3, 5, ..., all on the GPU.
+ * primes_out: HOST, want * s limbs, in candidate order; *tried_out (may be
+ * NULL) = candidates examined.  Synchronous.  Errors: RSA_ERANGE, RSA_EINVAL,
+ * RSA_ECUDA. */
+int rsa_prime_search(int nbits, uint64_t seed, int want, int rounds, uint32_t* primes_out,
+                     unsigned long long* tried_out);
+
+/* Key generation, Fig 1: p, q from rsa_prime_search (seeded),
+ * then rsa_keygen_check (host Miller-Rabin re-test, gcd(e, phi) = 1, d).
+ * 32 <= nbits <= 4096; p has nbits/2 bits, q nbits - nbits/2 bits, so n has
+ * exactly nbits bits.  HOST outputs: p_out, q_out with h = ceil((nbits -
+ * nbits/2)/32) limbs; n_out, phi_out, d_out with 2h limbs.  Synchronous. */
+int rsa_keygen(int nbits, const uint32_t* e, int e_limbs, uint64_t seed, uint32_t* p_out, uint32_t* q_out,
+               uint32_t* n_out, uint32_t* phi_out, uint32_t* d_out);
+
 /* Plan summary for (exp, n, nbits): the width class, window and the number
  * of Montgomery multiplications each packet costs (for the roofline). */
 typedef struct {

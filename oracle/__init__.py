@@ -63,6 +63,8 @@ def lib():
         L.oracle_validate_key.argtypes = [u32p, u32p, u32p, u32p, ctypes.c_int, u32p]
         L.oracle_modexp_batch.argtypes = [u32p, ctypes.c_size_t, ctypes.c_int, u32p, ctypes.c_int,
                                           u32p, ctypes.c_int, u32p, ctypes.c_int]
+        L.oracle_modexp_multi.argtypes = [u32p, u32p, u32p, ctypes.c_size_t, ctypes.c_int, u32p, ctypes.c_int]
+        L.oracle_mr_round.argtypes = [u32p, ctypes.c_int, ctypes.c_uint32]
         L.oracle_encode.argtypes = [ctypes.c_char_p, u32p, ctypes.c_size_t, ctypes.POINTER(ctypes.c_size_t)]
         L.oracle_decode.argtypes = [u32p, ctypes.c_size_t, ctypes.c_char_p, ctypes.c_size_t]
         _lib = L
@@ -161,6 +163,29 @@ def modexp_batch(base: np.ndarray, e: int, m: int, nthreads: int | None = None) 
     if rc:
         raise OracleError(rc, "modexp_batch")
     return out
+
+
+def modexp_multi(base: np.ndarray, exps: np.ndarray, mods: np.ndarray, nthreads: int | None = None) -> np.ndarray:
+    """out[i] = base[i]^exps[i] mod mods[i] (all uint32 [count, s])."""
+    base = np.ascontiguousarray(base, dtype=np.uint32)
+    exps = np.ascontiguousarray(exps, dtype=np.uint32)
+    mods = np.ascontiguousarray(mods, dtype=np.uint32)
+    count, s = base.shape
+    assert exps.shape == mods.shape == base.shape
+    out = np.zeros((count, s), dtype=np.uint32)
+    rc = lib().oracle_modexp_multi(_p(base), _p(exps), _p(mods), count, s, _p(out), nthreads or os.cpu_count() or 1)
+    if rc:
+        raise OracleError(rc, "modexp_multi")
+    return out
+
+
+def mr_round(n: int, a: int) -> bool:
+    """One Miller-Rabin round to base a (strong probable prime test)."""
+    N = limbs_of(n)
+    rc = lib().oracle_mr_round(_p(N), len(N), a)
+    if rc < 0:
+        raise OracleError(rc, "mr_round")
+    return rc == 1
 
 
 # ---------------------------------------------------------------- keys

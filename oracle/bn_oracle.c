@@ -960,3 +960,89 @@ int oracle_decode(const uint32_t *packets, size_t count, char *text, size_t cap)
     text[2 * count] = 0;
     return OR_OK;
 }
+
+/* ---------------- multi-key batch: per-packet exponent and modulus ------------- */
+
+typedef struct {
+    const uint32_t *base, *exps, *mods;
+    int s;
+    uint32_t *out;
+    size_t lo, hi;
+} multi_job_t;
+
+static void *multi_worker(void *arg)
+{
+    multi_job_t *jb = (multi_job_t *)arg;
+    size_t i;
+    for (i = jb->lo; i < jb->hi; i++) {
+        bn_t G, E, M, A;
+        bn_from_limbs(&G, jb->base + i * (size_t)jb->s, jb->s);
+        bn_from_limbs(&E, jb->exps + i * (size_t)jb->s, jb->s);
+        bn_from_limbs(&M, jb->mods + i * (size_t)jb->s, jb->s);
+        if (bn_is_zero(&M)) {
+            bn_zero(&A);
+        } else {
+            bn_modexp_l2r(&A, &G, &E, &M);       /* Fig 5 */
+        }
+        bn_to_limbs(jb->out + i * (size_t)jb->s, jb->s, &A);
+    }
+    return NULL;
+}
+
+/* out[i] = base[i]^exps[i] mod mods[i]; all [count][s] limbs. */
+int oracle_modexp_multi(const uint32_t *base, const uint32_t *exps, const uint32_t *mods, size_t count,
+                        int s, uint32_t *out, int nthreads)
+{
+    pthread_t *th;
+    multi_job_t *jobs;
+    int t;
+    size_t per;
+    CHECK_LEN(s);
+    if (nthreads < 1)
+        nthreads = 1;
+    if ((size_t)nthreads > count)
+        nthreads = count ? (int)count : 1;
+    th = (pthread_t *)malloc(sizeof(pthread_t) * (size_t)nthreads);
+    jobs = (multi_job_t *)malloc(sizeof(multi_job_t) * (size_t)nthreads);
+    per = (count + (size_t)nthreads - 1) / (size_t)nthreads;
+    for (t = 0; t < nthreads; t++) {
+        jobs[t].base = base;
+        jobs[t].exps = exps;
+        jobs[t].mods = mods;
+        jobs[t].s = s;
+        jobs[t].out = out;
+        jobs[t].lo = (size_t)t * per < count ? (size_t)t * per : count;
+        jobs[t].hi = (size_t)(t + 1) * per < count ? (size_t)(t + 1) * per : count;
+        pthread_create(&th[t], NULL, multi_worker, &jobs[t]);
+    }
+    for (t = 0; t < nthreads; t++)
+        pthread_join(th[t], NULL);
+    free(th);
+    free(jobs);
+    return OR_OK;
+}
+
+/* One Miller-Rabin round to base a on odd n >= 5: returns 1 if n is a strong
+ * probable prime to base a (n - 1 = 2^r q, a^q = 1 or a^(2^j q) = n - 1 for
+ * some j < r), else 0. */
+int oracle_mr_round(const uint32_t *n, int nl, uint32_t a)
+{
+    bn_t N, one, nm1, q, A;
+    int r;
+    if (nl < 1 || nl > 128)
+        return OR_EINVAL;
+    bn_from_limbs(&N, n, nl);
+    bn_set_u32(&one, 1);
+    bn_sub(&nm1, &N, &one);
+    bn_copy(&q, &nm1);
+    r = 0;
+    while (!bn_bit(&q, 0)) {
+        int k;
+        for (k = 0; k < q.len; k++)
+            q.d[k] = (q.d[k] >> 1) | (k + 1 < q.len ? (q.d[k + 1] << 31) : 0u);
+        bn_norm(&q);
+        r++;
+    }
+    bn_set_u32(&A, a);
+    return mr_round(&N, &nm1, &q, r, &A);
+}

@@ -30,7 +30,8 @@ RSA_MAX_NBITS = 4096
 
 EXPORTS = ["rsa_strerror", "rsa_keygen_check", "rsa_validate_key", "rsa_modexp_batch",
            "rsa_modexp_batch_host", "rsa_plan_info", "rsa_set_window", "rsa_encode", "rsa_decode",
-           "rsa_kernel_launches", "rsa_modexp_batch_paper"]
+           "rsa_kernel_launches", "rsa_modexp_batch_paper", "rsa_modexp_batch_multi", "rsa_miller_rabin_batch",
+           "rsa_prime_candidates", "rsa_prime_sieve", "rsa_prime_search", "rsa_keygen"]
 
 if not os.path.exists(LIB_PATH):
     raise ImportError(f"{LIB_PATH} is not built: run `python -m paper_1407_1465_b200.build` "
@@ -60,6 +61,14 @@ _lib.rsa_set_window.argtypes = [ctypes.c_int]
 _lib.rsa_encode.argtypes = [ctypes.c_char_p, _u32p, ctypes.c_size_t, ctypes.POINTER(ctypes.c_size_t)]
 _lib.rsa_decode.argtypes = [_u32p, ctypes.c_size_t, ctypes.c_char_p, ctypes.c_size_t]
 _lib.rsa_kernel_launches.restype = ctypes.c_ulonglong
+_vp = ctypes.c_void_p
+_lib.rsa_modexp_batch_multi.argtypes = [_vp, _vp, _vp, ctypes.c_int, ctypes.c_int, ctypes.c_size_t, _vp, _vp, _vp]
+_lib.rsa_miller_rabin_batch.argtypes = [_vp, ctypes.c_int, ctypes.c_size_t, ctypes.c_uint32, _vp, _vp]
+_lib.rsa_prime_candidates.argtypes = [ctypes.c_int, ctypes.c_uint64, ctypes.c_ulonglong, ctypes.c_size_t, _vp, _vp]
+_lib.rsa_prime_sieve.argtypes = [_vp, ctypes.c_int, ctypes.c_size_t, _vp, _vp]
+_lib.rsa_prime_search.argtypes = [ctypes.c_int, ctypes.c_uint64, ctypes.c_int, ctypes.c_int, _u32p,
+                                  ctypes.POINTER(ctypes.c_ulonglong)]
+_lib.rsa_keygen.argtypes = [ctypes.c_int, _u32p, ctypes.c_int, ctypes.c_uint64, _u32p, _u32p, _u32p, _u32p, _u32p]
 _lib.rsa_modexp_batch_paper.argtypes = [ctypes.c_void_p, ctypes.c_uint64, ctypes.c_uint32, ctypes.c_size_t,
                                         ctypes.c_void_p, ctypes.c_int, ctypes.c_void_p]
 
@@ -156,6 +165,85 @@ def rsa_modexp_batch_paper(num, key: int, den: int, faithful: bool = True, out=N
                                          ctypes.c_void_p(out.data_ptr()), 1 if faithful else 0, ctypes.c_void_p(stream))
     _check(rc, "rsa_modexp_batch_paper")
     return out
+
+
+def _stream_of(t, stream):
+    import torch
+    if stream is None:
+        return torch.cuda.current_stream(t.device).cuda_stream
+    return stream.cuda_stream if hasattr(stream, "cuda_stream") else stream
+
+
+def rsa_modexp_batch_multi(base, exps, mods, nbits: int, exp_bits: int | None = None, out=None, status=None,
+                           stream=None):
+    """out[i] = base[i]^exps[i] mod mods[i] (CUDA [count, s] 32-bit tensors)."""
+    import torch
+    s = nlimbs(nbits)
+    for t in (base, exps, mods):
+        if t.dim() != 2 or t.shape[1] != s or not t.is_cuda or t.shape != base.shape:
+            raise ValueError(f"base/exps/mods must be CUDA [count, {s}] tensors")
+    base, exps, mods = base.contiguous(), exps.contiguous(), mods.contiguous()
+    if out is None:
+        out = torch.empty_like(base)
+    exp_bits = 32 * s if exp_bits is None else exp_bits
+    with torch.cuda.device(base.device):
+        rc = _lib.rsa_modexp_batch_multi(_vp(base.data_ptr()), _vp(exps.data_ptr()), _vp(mods.data_ptr()), nbits,
+                                         exp_bits, base.shape[0], _vp(out.data_ptr()),
+                                         _vp(status.data_ptr() if status is not None else 0),
+                                         _vp(_stream_of(base, stream)))
+    _check(rc, "rsa_modexp_batch_multi")
+    return out
+
+
+def rsa_miller_rabin_batch(cand, nbits: int, base: int, out=None, stream=None):
+    import torch
+    cand = cand.contiguous()
+    if out is None:
+        out = torch.empty(cand.shape[0], dtype=torch.int32, device=cand.device)
+    with torch.cuda.device(cand.device):
+        rc = _lib.rsa_miller_rabin_batch(_vp(cand.data_ptr()), nbits, cand.shape[0], base, _vp(out.data_ptr()),
+                                         _vp(_stream_of(cand, stream)))
+    _check(rc, "rsa_miller_rabin_batch")
+    return out
+
+
+def rsa_prime_candidates(nbits: int, seed: int, first: int, count: int, device="cuda", stream=None):
+    import torch
+    out = torch.empty((count, nlimbs(nbits)), dtype=torch.int32, device=device)
+    with torch.cuda.device(out.device):
+        rc = _lib.rsa_prime_candidates(nbits, seed, first, count, _vp(out.data_ptr()), _vp(_stream_of(out, stream)))
+    _check(rc, "rsa_prime_candidates")
+    return out
+
+
+def rsa_prime_sieve(cand, nbits: int, stream=None):
+    import torch
+    cand = cand.contiguous()
+    out = torch.empty(cand.shape[0], dtype=torch.int32, device=cand.device)
+    with torch.cuda.device(cand.device):
+        rc = _lib.rsa_prime_sieve(_vp(cand.data_ptr()), nbits, cand.shape[0], _vp(out.data_ptr()),
+                                  _vp(_stream_of(cand, stream)))
+    _check(rc, "rsa_prime_sieve")
+    return out
+
+
+def rsa_prime_search(nbits: int, seed: int, want: int, rounds: int = 8):
+    """Returns (primes as Python ints, candidates tried)."""
+    s = nlimbs(nbits)
+    buf = np.zeros(max(want, 1) * s, np.uint32)
+    tried = ctypes.c_ulonglong(0)
+    _check(_lib.rsa_prime_search(nbits, seed, want, rounds, _p(buf), ctypes.byref(tried)), "rsa_prime_search")
+    return [to_int(buf[i * s:(i + 1) * s]) for i in range(want)], tried.value
+
+
+def rsa_keygen(nbits: int, e: int = 65537, seed: int = 1):
+    """Fig 1 key generation with the GPU prime search -> dict(p, q, n, phi, d, e)."""
+    h = nlimbs(nbits - nbits // 2)
+    el = nlimbs(max(e.bit_length(), 1))
+    P, Q = np.zeros(h, np.uint32), np.zeros(h, np.uint32)
+    N, PHI, D = (np.zeros(2 * h, np.uint32) for _ in range(3))
+    _check(_lib.rsa_keygen(nbits, _p(limbs(e, el)), el, seed, _p(P), _p(Q), _p(N), _p(PHI), _p(D)), "rsa_keygen")
+    return dict(p=to_int(P), q=to_int(Q), n=to_int(N), phi=to_int(PHI), d=to_int(D), e=e)
 
 
 def rsa_plan_info(exp: int, n: int, nbits: int) -> dict:

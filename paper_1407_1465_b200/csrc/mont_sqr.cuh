@@ -51,9 +51,9 @@ __device__ __forceinline__ void mac3(uint32_t& c0, uint32_t& c1, uint32_t& c2, u
     addc(c2, c2, 0u);
 }
 
+// T = a^2 (2S limbs): steps 1-3 above (independent of the modulus)
 template <int S>
-__device__ __forceinline__ void montsqr(uint32_t (&a)[S], const uint32_t* __restrict__ n, uint32_t n0inv) {
-    uint32_t T[2 * S];
+__device__ __forceinline__ void square_full(const uint32_t (&a)[S], uint32_t (&T)[2 * S]) {
     // 1. off-diagonal triangle, product scanning
     uint32_t c0 = 0, c1 = 0, c2 = 0;
     T[0] = 0;
@@ -89,6 +89,12 @@ __device__ __forceinline__ void montsqr(uint32_t (&a)[S], const uint32_t* __rest
         madc_lo_cc(T[2 * i], a[i], a[i], T[2 * i]);
         madc_hi_cc(T[2 * i + 1], a[i], a[i], T[2 * i + 1]);
     }
+}
+
+template <int S>
+__device__ __forceinline__ void montsqr(uint32_t (&a)[S], const uint32_t* __restrict__ n, uint32_t n0inv) {
+    uint32_t T[2 * S];
+    square_full<S>(a, T);
     // 4. reduce T_low
     uint32_t X[S], Y[S], hi = 0;
 #pragma unroll

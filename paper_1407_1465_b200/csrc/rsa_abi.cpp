@@ -10,6 +10,7 @@
 #include <stdint.h>
 #include <string.h>
 
+#include <algorithm>
 #include <atomic>
 #include <map>
 #include <mutex>
@@ -24,6 +25,14 @@ cudaError_t rsa_b200_launch(int S, const void* params, int sms, cudaStream_t str
 cudaError_t rsa_b200_grid(int S, int sms, int* grid, int* block, size_t* nthreads);
 size_t rsa_b200_params_size(int S);
 cudaError_t rsa_b200_fill_one(uint32_t* out, unsigned long long count, int s_io, int sms, cudaStream_t stream);
+cudaError_t rsa_b200_multi(int S, const uint32_t* base, const uint32_t* exps, const uint32_t* mods, uint32_t* out,
+                           int32_t* status, void* table, unsigned long long count, int s_io, int exp_bits,
+                           int window, int mode, uint32_t mr_base, int sms, cudaStream_t stream, size_t* slots,
+                           bool query_only);
+cudaError_t rsa_b200_prime_candidates(uint64_t seed, unsigned long long first, unsigned long long count, int nbits,
+                                      int s_io, uint32_t* out, cudaStream_t stream);
+cudaError_t rsa_b200_sieve(const uint32_t* cand, unsigned long long count, int s_io, uint32_t* verdict,
+                           cudaStream_t stream);
 cudaError_t rsa_b200_paper_fig12(const uint32_t* num, uint64_t key, uint32_t den, unsigned long long count,
                                  int faithful, uint32_t* result, cudaStream_t stream);
 
@@ -297,6 +306,51 @@ static int enqueue(const Plan& pl, const uint32_t* base, uint32_t* out, size_t c
     return RSA_OK;
 }
 
+
+// ------------------------------------------------------------------ f1: multi-key, MR, prime search
+
+static int multi_class(int s_io) {
+    int c = width_class(s_io);
+    if (c && c < 8) c = 8;
+    return (c && c <= 64) ? c : 0;
+}
+
+// fixed window minimising bits + bits/w + 2^w
+static int multi_window(int bits) {
+    int best = 1;
+    double bc = 1e30;
+    for (int w = 1; w <= 6; w++) {
+        const double c = bits + (double)bits / w + (1 << w);
+        if (c < bc) { bc = c; best = w; }
+    }
+    return best;
+}
+
+static int enqueue_multi(const uint32_t* base, const uint32_t* exps, const uint32_t* mods, int nbits, int exp_bits,
+                         size_t count, uint32_t* out, int32_t* status, int mode, uint32_t mr_base,
+                         cudaStream_t stream) {
+    const int s_io = (nbits + 31) / 32;
+    const int S = multi_class(s_io);
+    if (!S) return RSA_ERANGE;
+    const int sms = device_sms();
+    if (!sms) return RSA_ECUDA;
+    const int w = multi_window(exp_bits);
+    size_t slots = 0;
+    if (rsa_b200_multi(S, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, 0, s_io, exp_bits, w, mode, mr_base,
+                       sms, stream, &slots, true) != cudaSuccess)
+        return RSA_ECUDA;
+    keep_pool_memory();
+    void* table = nullptr;
+    const size_t tbytes = ((size_t)1 << w) * S * sizeof(uint32_t) * slots;
+    if (cudaMallocAsync(&table, tbytes, stream) != cudaSuccess) return RSA_ECUDA;
+    cudaError_t e = rsa_b200_multi(S, base, exps, mods, out, status, table, count, s_io, exp_bits, w, mode, mr_base,
+                                   sms, stream, nullptr, false);
+    cudaFreeAsync(table, stream);
+    if (e != cudaSuccess) return RSA_ECUDA;
+    g_launches++;
+    return RSA_OK;
+}
+
 }  // namespace
 
 extern "C" {
@@ -439,6 +493,145 @@ int rsa_modexp_batch_paper(const uint32_t* num, uint64_t key, uint32_t den, size
         return RSA_ECUDA;
     g_launches++;
     return RSA_OK;
+}
+
+
+int rsa_modexp_batch_multi(const uint32_t* base, const uint32_t* exps, const uint32_t* mods, int nbits, int exp_bits,
+                           size_t count, uint32_t* out, int32_t* status, void* stream) {
+    if (nbits < 2 || nbits > 2048) return RSA_ERANGE;
+    const int s_io = (nbits + 31) / 32;
+    if (exp_bits < 1 || exp_bits > 32 * s_io) return RSA_ERANGE;
+    if (count == 0) return RSA_OK;
+    if (!base || !exps || !mods || !out) return RSA_EINVAL;
+    return enqueue_multi(base, exps, mods, nbits, exp_bits, count, out, status, 0, 0, (cudaStream_t)stream);
+}
+
+int rsa_miller_rabin_batch(const uint32_t* cand, int nbits, size_t count, uint32_t base, uint32_t* verdict,
+                           void* stream) {
+    if (nbits < 4 || nbits > 2048) return RSA_ERANGE;
+    if (base < 2) return RSA_EINVAL;
+    if (count == 0) return RSA_OK;
+    if (!cand || !verdict) return RSA_EINVAL;
+    const int s_io = (nbits + 31) / 32;
+    return enqueue_multi(nullptr, nullptr, cand, nbits, 32 * s_io - 1, count, verdict, nullptr, 1, base,
+                         (cudaStream_t)stream);
+}
+
+int rsa_prime_candidates(int nbits, uint64_t seed, unsigned long long first, size_t count, uint32_t* out,
+                         void* stream) {
+    if (nbits < 4 || nbits > 2048) return RSA_ERANGE;
+    if (count == 0) return RSA_OK;
+    if (!out) return RSA_EINVAL;
+    const int s_io = (nbits + 31) / 32;
+    if (rsa_b200_prime_candidates(seed, first, count, nbits, s_io, out, (cudaStream_t)stream) != cudaSuccess)
+        return RSA_ECUDA;
+    g_launches++;
+    return RSA_OK;
+}
+
+int rsa_prime_sieve(const uint32_t* cand, int nbits, size_t count, uint32_t* verdict, void* stream) {
+    if (nbits < 4 || nbits > 2048) return RSA_ERANGE;
+    if (count == 0) return RSA_OK;
+    if (!cand || !verdict) return RSA_EINVAL;
+    if (rsa_b200_sieve(cand, count, (nbits + 31) / 32, verdict, (cudaStream_t)stream) != cudaSuccess)
+        return RSA_ECUDA;
+    g_launches++;
+    return RSA_OK;
+}
+
+// Search primes of exactly nbits bits (top two bits set): candidates from the
+// counter-based generator (index order), small-prime sieve and `rounds`
+// Miller-Rabin rounds (bases 2, 3, 5, 7, ...) on the GPU; the host only
+// compacts survivor lists.  Writes `want` primes (want * s limbs) in candidate
+// order; *tried_out = candidates examined.  Synchronous.
+int rsa_prime_search(int nbits, uint64_t seed, int want, int rounds, uint32_t* primes_out,
+                     unsigned long long* tried_out) {
+    static const uint32_t bases[] = {2, 3, 5, 7, 11, 13, 17, 19, 23, 29, 31, 37, 41, 43, 47, 53};
+    if (nbits < 16 || nbits > 2048) return RSA_ERANGE;
+    if (want < 0 || !primes_out || rounds < 1 || rounds > 16) return RSA_EINVAL;
+    if (want == 0) return RSA_OK;
+    const int s = (nbits + 31) / 32;
+    const size_t B = nbits <= 256 ? 16384 : 65536;
+    cudaStream_t st;
+    if (cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking) != cudaSuccess) return RSA_ECUDA;
+    uint32_t *d_cand = nullptr, *d_surv = nullptr, *d_ver = nullptr;
+    int rc = RSA_OK;
+    if (cudaMalloc(&d_cand, B * s * 4) != cudaSuccess || cudaMalloc(&d_surv, B * s * 4) != cudaSuccess ||
+        cudaMalloc(&d_ver, B * 4) != cudaSuccess)
+        rc = RSA_ECUDA;
+    std::vector<uint32_t> h_cand(B * s), h_surv, h_ver(B);
+    int found = 0;
+    unsigned long long first = 0;
+    while (rc == RSA_OK && found < want) {
+        if (rsa_b200_prime_candidates(seed, first, B, nbits, s, d_cand, st) != cudaSuccess ||
+            rsa_b200_sieve(d_cand, B, s, d_ver, st) != cudaSuccess) { rc = RSA_ECUDA; break; }
+        g_launches += 2;
+        if (cudaMemcpyAsync(h_cand.data(), d_cand, B * s * 4, cudaMemcpyDeviceToHost, st) != cudaSuccess ||
+            cudaMemcpyAsync(h_ver.data(), d_ver, B * 4, cudaMemcpyDeviceToHost, st) != cudaSuccess ||
+            cudaStreamSynchronize(st) != cudaSuccess) { rc = RSA_ECUDA; break; }
+        std::vector<size_t> idx;
+        for (size_t i = 0; i < B; i++)
+            if (h_ver[i]) idx.push_back(i);
+        for (int r = 0; r < rounds && !idx.empty(); r++) {
+            h_surv.resize(idx.size() * s);
+            for (size_t k = 0; k < idx.size(); k++)
+                memcpy(&h_surv[k * s], &h_cand[idx[k] * s], s * 4);
+            if (cudaMemcpyAsync(d_surv, h_surv.data(), idx.size() * s * 4, cudaMemcpyHostToDevice, st) != cudaSuccess) {
+                rc = RSA_ECUDA;
+                break;
+            }
+            rc = enqueue_multi(nullptr, nullptr, d_surv, nbits, 32 * s - 1, idx.size(), d_ver, nullptr, 1, bases[r], st);
+            if (rc) break;
+            if (cudaMemcpyAsync(h_ver.data(), d_ver, idx.size() * 4, cudaMemcpyDeviceToHost, st) != cudaSuccess ||
+                cudaStreamSynchronize(st) != cudaSuccess) { rc = RSA_ECUDA; break; }
+            std::vector<size_t> next;
+            for (size_t k = 0; k < idx.size(); k++)
+                if (h_ver[k]) next.push_back(idx[k]);
+            idx.swap(next);
+        }
+        for (size_t k = 0; rc == RSA_OK && k < idx.size() && found < want; k++, found++)
+            memcpy(primes_out + (size_t)found * s, &h_cand[idx[k] * s], s * 4);
+        first += B;
+    }
+    if (tried_out) *tried_out = first;
+    cudaFree(d_cand);
+    cudaFree(d_surv);
+    cudaFree(d_ver);
+    cudaStreamDestroy(st);
+    return rc;
+}
+
+// Fig 1 end to end: two different random primes from the GPU
+// search (p from seed, q from seed + 1), n = p q, phi, d = e^-1 mod phi via
+// rsa_keygen_check (which re-tests primality on the host).  p, q have
+// nbits/2 and nbits - nbits/2 bits with the top two bits set, so n has exactly
+// nbits bits.  Outputs: p_out, q_out (s_half limbs each, s_half =
+// ceil((nbits - nbits/2)/32)), n_out, phi_out, d_out (2 * s_half limbs each).
+int rsa_keygen(int nbits, const uint32_t* e, int e_limbs, uint64_t seed, uint32_t* p_out, uint32_t* q_out,
+               uint32_t* n_out, uint32_t* phi_out, uint32_t* d_out) {
+    if (nbits < 32 || nbits > 4096) return RSA_ERANGE;
+    if (!e || !p_out || !q_out || !n_out || !phi_out || !d_out || e_limbs < 1 || e_limbs > 128) return RSA_EINVAL;
+    const int bp = nbits / 2, bq = nbits - nbits / 2;
+    const int sh = (bq + 31) / 32;
+    std::vector<uint32_t> P(sh, 0), Q(sh, 0);
+    for (int attempt = 0; attempt < 64; attempt++) {
+        std::vector<uint32_t> pp((bp + 31) / 32), qq(sh);
+        int rc = rsa_prime_search(bp, seed + 2 * attempt, 1, 8, pp.data(), nullptr);
+        if (rc) return rc;
+        rc = rsa_prime_search(bq, seed + 2 * attempt + 1, 1, 8, qq.data(), nullptr);
+        if (rc) return rc;
+        std::fill(P.begin(), P.end(), 0u);
+        std::copy(pp.begin(), pp.end(), P.begin());
+        Q = qq;
+        rc = rsa_keygen_check(P.data(), Q.data(), sh, e, e_limbs, n_out, phi_out, d_out);
+        if (rc == RSA_OK) {
+            std::copy(P.begin(), P.end(), p_out);
+            std::copy(Q.begin(), Q.end(), q_out);
+            return RSA_OK;
+        }
+        if (rc != RSA_ENOTCOPRIME && rc != RSA_EEQUAL) return rc;
+    }
+    return RSA_ENOTCOPRIME;
 }
 
 int rsa_set_window(int w) {

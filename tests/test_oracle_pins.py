@@ -334,3 +334,39 @@ def test_workload_packets_below_n():
         assert max(vals[16:]) < 2 ** (k["nbits"] - 1)
         # deterministic
         assert np.array_equal(pk, workload.packets(4096, k["nbits"], n=k["n"], config_id=1))
+
+
+# ------------------------------------------------------------------ f1 oracle helpers
+
+def test_mr_round_known_strong_pseudoprimes():
+    """Strong pseudoprimes from the literature: 2047 (base 2), 1373653 (2, 3),
+    25326001 (2, 3, 5), 3215031751 (2, 3, 5, 7) -- each passes exactly those
+    bases and fails the next prime base."""
+    table = {2047: [2], 1373653: [2, 3], 25326001: [2, 3, 5], 3215031751: [2, 3, 5, 7]}
+    for n, ok in table.items():
+        for a in ok:
+            assert oracle.mr_round(n, a)
+        nxt = {1: 3, 2: 5, 3: 7, 4: 11}[len(ok)]
+        assert not oracle.mr_round(n, nxt)
+    for p in [1000003, 2 ** 61 - 1, 2 ** 127 - 1]:
+        assert all(oracle.mr_round(p, a) for a in (2, 3, 5, 7, 11))
+
+
+def test_modexp_multi_matches_pow():
+    rnd = random.Random(21)
+    s = 8
+    mods = [rnd.getrandbits(256) | 1 | (1 << 255) for _ in range(200)]
+    base = [rnd.getrandbits(256) for _ in range(200)]
+    exps = [rnd.getrandbits(rnd.choice([1, 17, 256])) for _ in range(200)]
+    B, E, M = (workload.ints_to_rows(v, s) for v in (base, exps, mods))
+    got = workload.rows_to_ints(oracle.modexp_multi(B, E, M))
+    assert got == [pow(b, e, m) for b, e, m in zip(base, exps, mods)]
+
+
+def test_candidate_generator_spec():
+    """workload.prime_candidates: exactly nbits bits, top two bits and bit 0
+    set, deterministic, index-addressable."""
+    for nb in (64, 100, 1024):
+        c = workload.rows_to_ints(workload.prime_candidates(nb, 3, 10, 20))
+        assert all(v.bit_length() == nb and (v >> (nb - 2)) == 3 and v & 1 for v in c)
+        assert c[5:] == workload.rows_to_ints(workload.prime_candidates(nb, 3, 15, 15))

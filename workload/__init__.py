@@ -153,3 +153,33 @@ def paper_packets(count: int, seed: int = MASTER_SEED, config_id: int = 0, high:
 
 # sec. 2 of the paper: the worked message
 PAPER_TEXT = "parallel encryption"
+
+
+# ------------------------------------------------------------------ prime-search candidates
+
+_M64 = (1 << 64) - 1
+
+
+def _splitmix_mix(x: int) -> int:
+    x &= _M64
+    x = ((x ^ (x >> 30)) * 0xBF58476D1CE4E5B9) & _M64
+    x = ((x ^ (x >> 27)) * 0x94D049BB133111EB) & _M64
+    return x ^ (x >> 31)
+
+
+def prime_candidates(nbits: int, seed: int, first: int, count: int) -> np.ndarray:
+    """The counter-based candidate generator of the GPU prime search
+    (modexp_multi.cu), re-implemented independently: candidate i, limb pair j
+    = splitmix64 finaliser of seed + (i * 2^16 + j + 1) * 0x9E3779B97F4A7C15;
+    masked to nbits, bits nbits-1, nbits-2 and 0 set.  uint32 [count, s]."""
+    s = limbs_needed(nbits)
+    vals = []
+    for i in range(first, first + count):
+        x = 0
+        for j in range((s + 1) // 2):
+            z = _splitmix_mix(seed + ((i << 16) + j + 1) * 0x9E3779B97F4A7C15)
+            x |= z << (64 * j)
+        x &= (1 << nbits) - 1
+        x |= (3 << (nbits - 2)) | 1
+        vals.append(x)
+    return ints_to_rows(vals, s)
