@@ -40,6 +40,13 @@ WORKLOADS = {
     "rsa4096-dec": ("rsa4096", 256 << 10, [("dec_full_d", "d")]),
     "rsa4096-roundtrip": ("rsa4096", 256 << 10, [("enc_e65537", "e"), ("dec_full_d", "d")]),
     "u64-roundtrip": ("rsa64", 16 << 20, [("enc_e65537", "e"), ("dec_full_d", "d")]),
+    # every packet with its own (random odd, 2048-bit) modulus, e = 65537
+    "multikey2048-enc": ("rsa2048", 1 << 20, [("multi_enc_e65537", "multi:65537")]),
+    # f3: CRT decryption of 1M RSA-2048 ciphertexts (same result as full d)
+    "rsa2048-dec-crt": ("rsa2048", 1 << 20, [("dec_crt", "crt:d")]),
+    "rsa4096-dec-crt": ("rsa4096", 256 << 10, [("dec_crt", "crt:d")]),
+    # f1: one Miller-Rabin round (base 2) on 1M 1024-bit prime-search candidates
+    "mr1024": ("rsa2048", 1 << 20, [("mr_base2_1024", "mr:1024")]),
     "toy-roundtrip": ("toy17947", 9, [("enc_e131", "e"), ("dec_d14171", "d")]),
 }
 
@@ -200,18 +207,56 @@ def run_ours(args, rank, world, local_rank):
     nb, n = key["nbits"], key["n"]
     s = workload.limbs_needed(nb)
     # each rank: its own full-size batch (weak scaling); seeds differ per rank
-    base_np = workload.packets(count, nb, n=n, config_id=2 + 100 * rank)
-    base = torch.from_numpy(base_np.view(np.int32)).to(dev)
-    bufs = [base] + [torch.empty_like(base) for _ in legs]
+    kind = legs[0][1].split(":")[0] if ":" in legs[0][1] else "batch"
     stream = torch.cuda.current_stream(dev)
-    exps = [key[f] for _, f in legs]
-    plans = [R.rsa_plan_info(e, n, nb) for e in exps]
+    if kind == "mr":
+        nb = int(legs[0][1].split(":")[1])
+        s = workload.limbs_needed(nb)
+        base = R.rsa_prime_candidates(nb, workload.MASTER_SEED + rank, 0, count, device=dev)
+        base_np = None
+    else:
+        base_np = workload.packets(count, nb, n=n, config_id=2 + 100 * rank)
+        base = torch.from_numpy(base_np.view(np.int32)).to(dev)
+    bufs = [base] + [torch.empty_like(base) for _ in legs]
+    if kind == "batch":
+        exps = [key[f] for _, f in legs]
+        plans = [R.rsa_plan_info(e, n, nb) for e in exps]
+    elif kind == "multi":
+        ev = int(legs[0][1].split(":")[1])
+        rng = np.random.Generator(np.random.PCG64(workload.MASTER_SEED + 500 + rank))
+        mods_np = rng.integers(0, 2**32, (count, s), dtype=np.uint64).astype(np.uint32)
+        mods_np[:, 0] |= 1
+        mods_np[:, s - 1] |= np.uint32(1 << 31)
+        mods = torch.from_numpy(mods_np.view(np.int32)).to(dev)
+        expt = torch.from_numpy(workload.ints_to_rows([ev] * 1, s).view(np.int32)).to(dev).expand(count, s).contiguous()
+        exps = [ev]
+        plans = [R.rsa_multi_plan_info(nb, ev.bit_length())]
+    elif kind == "crt":
+        exps = [key["d"]]
+        p_, q_ = max(key["p"], key["q"]), min(key["p"], key["q"])
+        hb = 32 * workload.limbs_needed(p_.bit_length())
+        hp = R.rsa_plan_info(key["d"] % (p_ - 1), p_, hb)
+        hq = R.rsa_plan_info(key["d"] % (q_ - 1), q_, hb)
+        plans = [dict(hp, montmuls=hp["montmuls"] + hq["montmuls"], squarings=hp["squarings"] + hq["squarings"],
+                      products=hp["products"] + hq["products"], window=hp["window"], exp_bits=hp["exp_bits"])]
+    else:
+        exps = [0]
+        plans = [R.rsa_multi_plan_info(nb, 0, mr=True)]
+        mr_out = torch.empty(count, dtype=torch.int32, device=dev)
 
     def step(evs=None):
         for j, e in enumerate(exps):
             if evs is not None:
                 evs[j][0].record(stream)
-            R.rsa_modexp_batch(bufs[j], e, n, nb, out=bufs[j + 1], stream=stream)
+            if kind == "batch":
+                R.rsa_modexp_batch(bufs[j], e, n, nb, out=bufs[j + 1], stream=stream)
+            elif kind == "multi":
+                R.rsa_modexp_batch_multi(bufs[j], expt, mods, nb, exp_bits=e.bit_length(), out=bufs[j + 1],
+                                         stream=stream)
+            elif kind == "crt":
+                R.rsa_decrypt_crt_batch(bufs[j], key["p"], key["q"], key["d"], nb, out=bufs[j + 1], stream=stream)
+            else:
+                R.rsa_miller_rabin_batch(bufs[j], nb, 2, out=mr_out, stream=stream)
             if evs is not None:
                 evs[j][1].record(stream)
 
@@ -251,7 +296,7 @@ def run_ours(args, rank, world, local_rank):
 
     # ---- end to end through the public host API (pinned host buffers)
     e2e = None
-    if not args.no_e2e and rank == 0:
+    if not args.no_e2e and rank == 0 and kind == "batch":
         host_in = torch.from_numpy(base_np.view(np.int32)).pin_memory()
         host_mid = [torch.empty_like(host_in).pin_memory() for _ in legs]
         R.rsa_modexp_batch_host(host_in, exps[0], n, nb, out=host_mid[0])      # warm
@@ -293,7 +338,9 @@ def run_ours(args, rank, world, local_rank):
     roofline = {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "Tprod/s", "frac": achieved / peak,
                 "traffic": ncu_traffic(key_name, legs[dom][0], count),
                 "traffic_unit": "bytes per launch", "algorithmic_bytes": count * s * 4 * 2,
-                "kernel": (f"modexp_pair_kernel<{S}>" if S == 128 else f"modexp_kernel<{S}>") + f" ({legs[dom][0]})",
+                "kernel": ({"multi": f"modexp_multi_kernel<{S}>", "mr": f"modexp_multi_kernel<{S}> (MR mode)",
+                            "crt": f"2 x modexp_kernel<{S}> + crt_split/combine (half-width CRT legs; products of both)"}.get(
+                    kind, f"modexp_pair_kernel<{S}>" if S == 128 else f"modexp_kernel<{S}>")) + f" ({legs[dom][0]})",
                 "algorithmic": f"{plans[dom]['products']} 32x32->64 limb products/packet "
                                f"({plans[dom]['squarings']} squarings x "
                                f"{'1.5S^2+1.5S' if plans[dom]['sqr_kernel'] else '2S^2+S'} + "
@@ -311,7 +358,7 @@ def run_ours(args, rank, world, local_rank):
                            "products_per_packet": plans[j]["products"], "window": plans[j]["window"],
                            "exp_bits": plans[j]["exp_bits"]}
     cpu = None
-    if not args.no_cpu_baseline and world == 1:
+    if not args.no_cpu_baseline and world == 1 and kind == "batch":
         cpu = cpu_baseline(key, base_np, legs, args.cpu_seconds)
     line = {"metric": METRIC, "value": value, "unit": "modexp/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",

@@ -99,6 +99,19 @@ int rsa_modexp_batch(const uint32_t* base, const uint32_t* exp, const uint32_t* 
 int rsa_modexp_batch_host(const uint32_t* base_host, const uint32_t* exp, const uint32_t* n,
                           int nbits, size_t count, uint32_t* out_host);
 
+/* CRT decryption (beyond the paper): the same
+ * M = C^d mod n as rsa_modexp_batch with exp = d, computed from
+ * the primes: m1 = C^(d mod p-1) mod p, m2 = C^(d mod q-1) mod q, M = m2 + q *
+ * (q^-1 (m1 - m2) mod p).  ~4x fewer limb products than the full-width path.
+ *   c, out : DEVICE, [count][s], s = ceil(nbits/32), 8 <= nbits <= 4096; each
+ *            c[i] < n = p q (as for decryption); out != c unless equal.
+ *   p, q   : HOST, pq_limbs limbs each (1..64), odd, distinct, p q < 2^nbits;
+ *   d      : HOST, s limbs.  Asynchronous on `stream` (4 launches).
+ * Errors: RSA_EINVAL, RSA_ERANGE, RSA_EEVEN, RSA_EEQUAL, RSA_ENOTCOPRIME,
+ * RSA_ECUDA. */
+int rsa_decrypt_crt_batch(const uint32_t* c, const uint32_t* p, const uint32_t* q, int pq_limbs, const uint32_t* d,
+                          int nbits, size_t count, uint32_t* out, void* stream);
+
 /* The paper's own GPU kernel, for comparison:
  * Alg 1 / Fig 11 + Alg 2 / Fig 12, one thread
  * per packet, 64 threads per block, O(key) loop: result[i] = num[i]^key mod
@@ -176,6 +189,10 @@ typedef struct {
 } rsa_plan_info_t;
 
 int rsa_plan_info(const uint32_t* exp, const uint32_t* n, int nbits, rsa_plan_info_t* info);
+
+/* Work summary of rsa_modexp_batch_multi (mr = 0) / rsa_miller_rabin_batch
+ * (mr = 1) per packet: window, Montgomery multiplications, products. */
+int rsa_multi_plan_info(int nbits, int exp_bits, int mr, rsa_plan_info_t* info);
 
 /* Force a sliding-window width for subsequent calls on this thread
  * (0 = automatic, the default; 1..7 = fixed).  For tests and benchmarks. */

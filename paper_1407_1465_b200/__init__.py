@@ -31,7 +31,8 @@ RSA_MAX_NBITS = 4096
 EXPORTS = ["rsa_strerror", "rsa_keygen_check", "rsa_validate_key", "rsa_modexp_batch",
            "rsa_modexp_batch_host", "rsa_plan_info", "rsa_set_window", "rsa_encode", "rsa_decode",
            "rsa_kernel_launches", "rsa_modexp_batch_paper", "rsa_modexp_batch_multi", "rsa_miller_rabin_batch",
-           "rsa_prime_candidates", "rsa_prime_sieve", "rsa_prime_search", "rsa_keygen"]
+           "rsa_prime_candidates", "rsa_prime_sieve", "rsa_prime_search", "rsa_keygen", "rsa_multi_plan_info",
+           "rsa_decrypt_crt_batch"]
 
 if not os.path.exists(LIB_PATH):
     raise ImportError(f"{LIB_PATH} is not built: run `python -m paper_1407_1465_b200.build` "
@@ -69,6 +70,8 @@ _lib.rsa_prime_sieve.argtypes = [_vp, ctypes.c_int, ctypes.c_size_t, _vp, _vp]
 _lib.rsa_prime_search.argtypes = [ctypes.c_int, ctypes.c_uint64, ctypes.c_int, ctypes.c_int, _u32p,
                                   ctypes.POINTER(ctypes.c_ulonglong)]
 _lib.rsa_keygen.argtypes = [ctypes.c_int, _u32p, ctypes.c_int, ctypes.c_uint64, _u32p, _u32p, _u32p, _u32p, _u32p]
+_lib.rsa_multi_plan_info.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.POINTER(RsaPlanInfo)]
+_lib.rsa_decrypt_crt_batch.argtypes = [_vp, _u32p, _u32p, ctypes.c_int, _u32p, ctypes.c_int, ctypes.c_size_t, _vp, _vp]
 _lib.rsa_modexp_batch_paper.argtypes = [ctypes.c_void_p, ctypes.c_uint64, ctypes.c_uint32, ctypes.c_size_t,
                                         ctypes.c_void_p, ctypes.c_int, ctypes.c_void_p]
 
@@ -132,6 +135,23 @@ def rsa_modexp_batch(base, exp: int, n: int, nbits: int, out=None, stream=None):
         rc = _lib.rsa_modexp_batch(ctypes.c_void_p(base.data_ptr()), _p(E), _p(N), nbits, base.shape[0],
                                    ctypes.c_void_p(out.data_ptr()), ctypes.c_void_p(stream))
     _check(rc, "rsa_modexp_batch")
+    return out
+
+
+def rsa_decrypt_crt_batch(c, p: int, q: int, d: int, nbits: int, out=None, stream=None):
+    """M = c^d mod pq by the CRT (two half-width exponentiations + Garner)."""
+    import torch
+    s = nlimbs(nbits)
+    if c.dim() != 2 or c.shape[1] != s or not c.is_cuda:
+        raise ValueError(f"c must be a CUDA [count, {s}] tensor")
+    c = c.contiguous()
+    if out is None:
+        out = torch.empty_like(c)
+    pl = nlimbs(max(p.bit_length(), q.bit_length(), 1))
+    with torch.cuda.device(c.device):
+        rc = _lib.rsa_decrypt_crt_batch(_vp(c.data_ptr()), _p(limbs(p, pl)), _p(limbs(q, pl)), pl, _p(limbs(d, s)),
+                                        nbits, c.shape[0], _vp(out.data_ptr()), _vp(_stream_of(c, stream)))
+    _check(rc, "rsa_decrypt_crt_batch")
     return out
 
 
@@ -250,6 +270,12 @@ def rsa_plan_info(exp: int, n: int, nbits: int) -> dict:
     s = nlimbs(nbits)
     info = RsaPlanInfo()
     _check(_lib.rsa_plan_info(_p(limbs(exp, s)), _p(limbs(n, s)), nbits, ctypes.byref(info)), "rsa_plan_info")
+    return {f: getattr(info, f) for f, _ in RsaPlanInfo._fields_}
+
+
+def rsa_multi_plan_info(nbits: int, exp_bits: int, mr: bool = False) -> dict:
+    info = RsaPlanInfo()
+    _check(_lib.rsa_multi_plan_info(nbits, exp_bits, 1 if mr else 0, ctypes.byref(info)), "rsa_multi_plan_info")
     return {f: getattr(info, f) for f, _ in RsaPlanInfo._fields_}
 
 

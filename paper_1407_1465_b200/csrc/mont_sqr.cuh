@@ -91,10 +91,11 @@ __device__ __forceinline__ void square_full(const uint32_t (&a)[S], uint32_t (&T
     }
 }
 
+// a <- T R^-1 mod n for a 2S-limb T with T_high = T >> 32S < n (steps 3-4):
+// reduction-only CIOS steps on T_low, then + T_high, one conditional subtract.
 template <int S>
-__device__ __forceinline__ void montsqr(uint32_t (&a)[S], const uint32_t* __restrict__ n, uint32_t n0inv) {
-    uint32_t T[2 * S];
-    square_full<S>(a, T);
+__device__ __forceinline__ void reduce_wide(uint32_t (&a)[S], const uint32_t (&T)[2 * S],
+                                            const uint32_t* __restrict__ n, uint32_t n0inv) {
     // 4. reduce T_low
     uint32_t X[S], Y[S], hi = 0;
 #pragma unroll
@@ -136,6 +137,13 @@ __device__ __forceinline__ void montsqr(uint32_t (&a)[S], const uint32_t* __rest
     subc(keep, hi, 0u);
 #pragma unroll
     for (int k = 0; k < S; k++) a[k] = (X[k] & keep) | (a[k] & ~keep);
+}
+
+template <int S>
+__device__ __forceinline__ void montsqr(uint32_t (&a)[S], const uint32_t* __restrict__ n, uint32_t n0inv) {
+    uint32_t T[2 * S];
+    square_full<S>(a, T);
+    reduce_wide<S>(a, T, n, n0inv);
 }
 
 }  // namespace rsa_b200

@@ -33,6 +33,12 @@ cudaError_t rsa_b200_prime_candidates(uint64_t seed, unsigned long long first, u
                                       int s_io, uint32_t* out, cudaStream_t stream);
 cudaError_t rsa_b200_sieve(const uint32_t* cand, unsigned long long count, int s_io, uint32_t* verdict,
                            cudaStream_t stream);
+size_t rsa_b200_crt_params_size(int SH);
+void rsa_b200_crt_fill(int SH, void* raw, const uint32_t* c, uint32_t* cp, uint32_t* cq, uint32_t* out,
+                       unsigned long long count, int s_io, int sh_io, uint32_t pinv, uint32_t qinv32,
+                       const uint32_t* p, const uint32_t* q, const uint32_t* r2p, const uint32_t* r2q,
+                       const uint32_t* qinvR);
+cudaError_t rsa_b200_crt_launch(int SH, const void* raw, int which, unsigned long long count, cudaStream_t st);
 cudaError_t rsa_b200_paper_fig12(const uint32_t* num, uint64_t key, uint32_t den, unsigned long long count,
                                  int faithful, uint32_t* result, cudaStream_t stream);
 
@@ -351,6 +357,69 @@ static int enqueue_multi(const uint32_t* base, const uint32_t* exps, const uint3
     return RSA_OK;
 }
 
+
+// ------------------------------------------------------------------ f3: CRT decryption
+
+struct CrtKey {
+    int SH = 0, sh_io = 0;
+    std::vector<uint32_t> p, q, dp, dq, r2p, r2q, qinvR;
+    uint32_t pinv = 0, qinv32 = 0;
+};
+
+static std::mutex g_crt_mu;
+static std::map<std::string, CrtKey> g_crt;
+
+static int get_crt_key(const uint32_t* p, const uint32_t* q, int pq_limbs, const uint32_t* d, int nbits, CrtKey* out) {
+    const int s = (nbits + 31) / 32;
+    std::string key((const char*)&nbits, sizeof(int));
+    key.append((const char*)&pq_limbs, sizeof(int));
+    key.append((const char*)p, 4 * pq_limbs);
+    key.append((const char*)q, 4 * pq_limbs);
+    key.append((const char*)d, 4 * s);
+    {
+        std::lock_guard<std::mutex> lk(g_crt_mu);
+        auto it = g_crt.find(key);
+        if (it != g_crt.end()) { *out = it->second; return RSA_OK; }
+    }
+    BN P = rsa_host::from_limbs(p, pq_limbs), Q = rsa_host::from_limbs(q, pq_limbs), D = rsa_host::from_limbs(d, s);
+    if (P.empty() || Q.empty() || !(P[0] & 1u) || !(Q[0] & 1u) || rsa_host::bits(P) < 2 || rsa_host::bits(Q) < 2)
+        return RSA_EEVEN;
+    if (rsa_host::cmp(P, Q) == 0) return RSA_EEQUAL;
+    BN N = rsa_host::mul(P, Q);
+    if (rsa_host::bits(N) > nbits) return RSA_ERANGE;
+    CrtKey ck;
+    const int hb = std::max(rsa_host::bits(P), rsa_host::bits(Q));
+    ck.sh_io = (hb + 31) / 32;
+    int SH = width_class(ck.sh_io);
+    if (SH < 4) SH = 4;
+    if (SH > 64) return RSA_ERANGE;
+    ck.SH = SH;
+    // p > q is not required: m2 < q < 2p holds for same-length primes; make
+    // the p-side the larger one so the single conditional subtraction suffices
+    if (rsa_host::cmp(P, Q) < 0) std::swap(P, Q);
+    BN one{1u};
+    BN dp = rsa_host::mod(D, rsa_host::sub(P, one)), dq = rsa_host::mod(D, rsa_host::sub(Q, one));
+    BN qinv;
+    if (!rsa_host::inverse(rsa_host::mod(Q, P), P, &qinv)) return RSA_ENOTCOPRIME;
+    BN R = rsa_host::pow2_mod(32 * SH, P);
+    BN qinvR = rsa_host::mod(rsa_host::mul(qinv, R), P);
+    auto vec = [&](const BN& x) { std::vector<uint32_t> v(SH, 0); rsa_host::to_limbs(x, v.data(), SH); return v; };
+    ck.p = vec(P); ck.q = vec(Q);
+    ck.dp = vec(dp); ck.dq = vec(dq);
+    ck.r2p = vec(rsa_host::pow2_mod(64 * SH, P));
+    ck.r2q = vec(rsa_host::pow2_mod(64 * SH, Q));
+    ck.qinvR = vec(qinvR);
+    ck.pinv = rsa_host::neg_inv32(P[0]);
+    ck.qinv32 = rsa_host::neg_inv32(Q[0]);
+    {
+        std::lock_guard<std::mutex> lk(g_crt_mu);
+        if (g_crt.size() > 64) g_crt.clear();
+        g_crt[key] = ck;
+    }
+    *out = ck;
+    return RSA_OK;
+}
+
 }  // namespace
 
 extern "C" {
@@ -496,6 +565,43 @@ int rsa_modexp_batch_paper(const uint32_t* num, uint64_t key, uint32_t den, size
 }
 
 
+int rsa_multi_plan_info(int nbits, int exp_bits, int mr, rsa_plan_info_t* info) {
+    if (!info) return RSA_EINVAL;
+    if (nbits < 2 || nbits > 2048) return RSA_ERANGE;
+    const int s_io = (nbits + 31) / 32;
+    const int S = multi_class(s_io);
+    if (mr) exp_bits = 32 * s_io - 1;
+    if (exp_bits < 1 || exp_bits > 32 * s_io) return RSA_ERANGE;
+    const int w = multi_window(exp_bits);
+    const int nwin = (exp_bits + w - 1) / w;
+    int K = 0;
+    while ((1 << K) < 32 * S) K++;
+    // modexp_multi.cu step machine: K SQR (R^2), 1 MUL (to Montgomery),
+    // 2^w - 2 MUL (table), (nwin - 1) x (w SQR + 1 MUL) scan, then 1 MUL
+    // (from Montgomery) or, for Miller-Rabin, r - 1 SQR (r ~ 1 on average)
+    const long long sq = K + (long long)(nwin - 1) * w;
+    const long long mm = sq + 1 + ((1 << w) - 2) + (nwin - 1) + (mr ? 0 : 1);
+    memset(info, 0, sizeof(*info));
+    info->width_class = S;
+    info->s_io = s_io;
+    info->window = w;
+    info->table_entries = 1 << w;
+    info->montmuls = mm;
+    info->squarings = sq;
+    info->exp_bits = exp_bits;
+    info->sqr_kernel = 1;
+    const long long SS = S;
+    info->products = sq * ((3 * SS * SS + 3 * SS) / 2) + (mm - sq) * (2 * SS * SS + SS);
+    const int sms = device_sms();
+    size_t slots = 0;
+    if (sms && rsa_b200_multi(S, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, 0, s_io, exp_bits, w, mr ? 1 : 0,
+                              2, sms, 0, &slots, true) == cudaSuccess) {
+        info->block = S >= 64 ? 256 : 128;
+        info->grid = (int)(slots / info->block);
+    }
+    return RSA_OK;
+}
+
 int rsa_modexp_batch_multi(const uint32_t* base, const uint32_t* exps, const uint32_t* mods, int nbits, int exp_bits,
                            size_t count, uint32_t* out, int32_t* status, void* stream) {
     if (nbits < 2 || nbits > 2048) return RSA_ERANGE;
@@ -632,6 +738,51 @@ int rsa_keygen(int nbits, const uint32_t* e, int e_limbs, uint64_t seed, uint32_
         if (rc != RSA_ENOTCOPRIME && rc != RSA_EEQUAL) return rc;
     }
     return RSA_ENOTCOPRIME;
+}
+
+
+int rsa_decrypt_crt_batch(const uint32_t* c, const uint32_t* p, const uint32_t* q, int pq_limbs, const uint32_t* d,
+                          int nbits, size_t count, uint32_t* out, void* stream) {
+    if (!p || !q || !d) return RSA_EINVAL;
+    if (nbits < 8 || nbits > 4096 || pq_limbs < 1 || pq_limbs > 64) return RSA_ERANGE;
+    if (count == 0) return RSA_OK;
+    if (!c || !out) return RSA_EINVAL;
+    const int s = (nbits + 31) / 32;
+    const size_t bytes = count * (size_t)s * 4;
+    if ((const char*)c != (const char*)out && (const char*)c < (const char*)out + bytes &&
+        (const char*)out < (const char*)c + bytes)
+        return RSA_EINVAL;
+    CrtKey ck;
+    int st = get_crt_key(p, q, pq_limbs, d, nbits, &ck);
+    if (st) return st;
+    if (2 * ck.SH < s) return RSA_ERANGE;
+    const int hbits = 32 * ck.sh_io;
+    Plan pp, pq;
+    st = get_plan(ck.dp.data(), ck.p.data(), hbits, &pp);
+    if (st) return st;
+    st = get_plan(ck.dq.data(), ck.q.data(), hbits, &pq);
+    if (st) return st;
+    cudaStream_t cs = (cudaStream_t)stream;
+    keep_pool_memory();
+    uint32_t *cp = nullptr, *cq = nullptr;
+    const size_t hb = count * (size_t)ck.sh_io * 4;
+    if (cudaMallocAsync((void**)&cp, hb, cs) != cudaSuccess) return RSA_ECUDA;
+    if (cudaMallocAsync((void**)&cq, hb, cs) != cudaSuccess) { cudaFreeAsync(cp, cs); return RSA_ECUDA; }
+    std::vector<unsigned char> prm(rsa_b200_crt_params_size(ck.SH));
+    rsa_b200_crt_fill(ck.SH, prm.data(), c, cp, cq, out, count, s, ck.sh_io, ck.pinv, ck.qinv32, ck.p.data(),
+                      ck.q.data(), ck.r2p.data(), ck.r2q.data(), ck.qinvR.data());
+    int rc = RSA_OK;
+    if (rsa_b200_crt_launch(ck.SH, prm.data(), 0, count, cs) != cudaSuccess) rc = RSA_ECUDA;
+    else g_launches++;
+    if (!rc) rc = enqueue(pp, cp, cp, count, cs);      // m1 = (C mod p)^dp mod p
+    if (!rc) rc = enqueue(pq, cq, cq, count, cs);      // m2 = (C mod q)^dq mod q
+    if (!rc) {
+        if (rsa_b200_crt_launch(ck.SH, prm.data(), 1, count, cs) != cudaSuccess) rc = RSA_ECUDA;
+        else g_launches++;
+    }
+    cudaFreeAsync(cp, cs);
+    cudaFreeAsync(cq, cs);
+    return rc;
 }
 
 int rsa_set_window(int w) {
