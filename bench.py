@@ -45,6 +45,8 @@ WORKLOADS = {
     # f3: CRT decryption of 1M RSA-2048 ciphertexts (same result as full d)
     "rsa2048-dec-crt": ("rsa2048", 1 << 20, [("dec_crt", "crt:d")]),
     "rsa4096-dec-crt": ("rsa4096", 256 << 10, [("dec_crt", "crt:d")]),
+    # f4: sec. 2 text -> packets -> C -> M -> text, fused, toy key, 16M letters
+    "toy-text-roundtrip": ("toy17947", 8 << 20, [("enc_text_e131", "text:e"), ("dec_text_d14171", "text:d")]),
     # f1: one Miller-Rabin round (base 2) on 1M 1024-bit prime-search candidates
     "mr1024": ("rsa2048", 1 << 20, [("mr_base2_1024", "mr:1024")]),
     "toy-roundtrip": ("toy17947", 9, [("enc_e131", "e"), ("dec_d14171", "d")]),
@@ -155,6 +157,24 @@ def ncu_traffic(key_name: str, leg: str, count: int):
     return None if not rec else rec["bytes_per_packet"] * count
 
 
+def _lib_text_enc(R, letters, e, n, nb, out, stream):
+    import ctypes
+    s = R.nlimbs(nb)
+    rc = R._lib.rsa_encrypt_text(ctypes.c_void_p(letters.data_ptr()), letters.numel(), R._p(R.limbs(e, s)),
+                                 R._p(R.limbs(n, s)), nb, ctypes.c_void_p(out.data_ptr()), None,
+                                 ctypes.c_void_p(stream.cuda_stream))
+    R._check(rc, "rsa_encrypt_text")
+
+
+def _lib_text_dec(R, cipher, d, n, nb, out, stream):
+    import ctypes
+    s = R.nlimbs(nb)
+    rc = R._lib.rsa_decrypt_text(ctypes.c_void_p(cipher.data_ptr()), cipher.shape[0], R._p(R.limbs(d, s)),
+                                 R._p(R.limbs(n, s)), nb, ctypes.c_void_p(out.data_ptr()), None,
+                                 ctypes.c_void_p(stream.cuda_stream))
+    R._check(rc, "rsa_decrypt_text")
+
+
 # ------------------------------------------------------------------ arms
 
 def run_reference(args, rank, world):
@@ -209,7 +229,12 @@ def run_ours(args, rank, world, local_rank):
     # each rank: its own full-size batch (weak scaling); seeds differ per rank
     kind = legs[0][1].split(":")[0] if ":" in legs[0][1] else "batch"
     stream = torch.cuda.current_stream(dev)
-    if kind == "mr":
+    if kind == "text":
+        rng = np.random.default_rng(workload.MASTER_SEED + rank)
+        letters = torch.from_numpy((rng.integers(0, 26, 2 * count) + ord("a")).astype(np.uint8)).to(dev)
+        base = letters
+        base_np = None
+    elif kind == "mr":
         nb = int(legs[0][1].split(":")[1])
         s = workload.limbs_needed(nb)
         base = R.rsa_prime_candidates(nb, workload.MASTER_SEED + rank, 0, count, device=dev)
@@ -218,7 +243,11 @@ def run_ours(args, rank, world, local_rank):
         base_np = workload.packets(count, nb, n=n, config_id=2 + 100 * rank)
         base = torch.from_numpy(base_np.view(np.int32)).to(dev)
     bufs = [base] + [torch.empty_like(base) for _ in legs]
-    if kind == "batch":
+    if kind == "text":
+        bufs = [letters, torch.empty((count, s), dtype=torch.int32, device=dev), torch.empty_like(letters)]
+        exps = [key["e"], key["d"]]
+        plans = [R.rsa_plan_info(e, n, nb) for e in exps]
+    elif kind == "batch":
         exps = [key[f] for _, f in legs]
         plans = [R.rsa_plan_info(e, n, nb) for e in exps]
     elif kind == "multi":
@@ -253,6 +282,10 @@ def run_ours(args, rank, world, local_rank):
             elif kind == "multi":
                 R.rsa_modexp_batch_multi(bufs[j], expt, mods, nb, exp_bits=e.bit_length(), out=bufs[j + 1],
                                          stream=stream)
+            elif kind == "text" and j == 0:
+                _lib_text_enc(R, bufs[0], e, n, nb, bufs[1], stream)
+            elif kind == "text":
+                _lib_text_dec(R, bufs[1], e, n, nb, bufs[2], stream)
             elif kind == "crt":
                 R.rsa_decrypt_crt_batch(bufs[j], key["p"], key["q"], key["d"], nb, out=bufs[j + 1], stream=stream)
             else:

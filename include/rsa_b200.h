@@ -210,6 +210,23 @@ int rsa_set_window(int w);
 int rsa_encode(const char* text, uint32_t* packets, size_t cap, size_t* count_out);
 int rsa_decode(const uint32_t* packets, size_t count, char* text, size_t cap);
 
+/* ---- codec fused with the exponentiation ----
+ * rsa_encrypt_text: DEVICE `text` of nletters lowercase letters a..z (spaces
+ * already stripped, nletters even) -> cipher[i] = packet_i^e mod n, packet_i =
+ * hi*100 + lo of letters 2i, 2i+1, in one kernel.  cipher:
+ * DEVICE [nletters/2][s] limbs, s = ceil(nbits/32).  Single-word keys only:
+ * 2 <= nbits <= 64 and n > 2525 (every packet must be < n).
+ * rsa_decrypt_text: DEVICE cipher [count][s] -> packet = c^d mod n -> two
+ * letters per packet into DEVICE `text` (2*count bytes, no terminator).
+ * status (DEVICE int32 per packet, may be NULL): 0, RSA_ECHAR (a letter
+ * outside a..z; that packet encrypts 0) or RSA_EPACKET (a result that is not a
+ * packet; its letters are "??").  Asynchronous.  Errors: RSA_EINVAL,
+ * RSA_ERANGE, RSA_EEVEN, RSA_EODD, RSA_ECUDA. */
+int rsa_encrypt_text(const char* text, size_t nletters, const uint32_t* e, const uint32_t* n, int nbits,
+                     uint32_t* cipher, int* status, void* stream);
+int rsa_decrypt_text(const uint32_t* cipher, size_t count, const uint32_t* d, const uint32_t* n, int nbits,
+                     char* text, int* status, void* stream);
+
 /* Number of kernels this library has launched since load (for the bench's
  * gpu_launches accounting). */
 unsigned long long rsa_kernel_launches(void);

@@ -32,7 +32,7 @@ EXPORTS = ["rsa_strerror", "rsa_keygen_check", "rsa_validate_key", "rsa_modexp_b
            "rsa_modexp_batch_host", "rsa_plan_info", "rsa_set_window", "rsa_encode", "rsa_decode",
            "rsa_kernel_launches", "rsa_modexp_batch_paper", "rsa_modexp_batch_multi", "rsa_miller_rabin_batch",
            "rsa_prime_candidates", "rsa_prime_sieve", "rsa_prime_search", "rsa_keygen", "rsa_multi_plan_info",
-           "rsa_decrypt_crt_batch"]
+           "rsa_decrypt_crt_batch", "rsa_encrypt_text", "rsa_decrypt_text"]
 
 if not os.path.exists(LIB_PATH):
     raise ImportError(f"{LIB_PATH} is not built: run `python -m paper_1407_1465_b200.build` "
@@ -72,6 +72,8 @@ _lib.rsa_prime_search.argtypes = [ctypes.c_int, ctypes.c_uint64, ctypes.c_int, c
 _lib.rsa_keygen.argtypes = [ctypes.c_int, _u32p, ctypes.c_int, ctypes.c_uint64, _u32p, _u32p, _u32p, _u32p, _u32p]
 _lib.rsa_multi_plan_info.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.POINTER(RsaPlanInfo)]
 _lib.rsa_decrypt_crt_batch.argtypes = [_vp, _u32p, _u32p, ctypes.c_int, _u32p, ctypes.c_int, ctypes.c_size_t, _vp, _vp]
+_lib.rsa_encrypt_text.argtypes = [_vp, ctypes.c_size_t, _u32p, _u32p, ctypes.c_int, _vp, _vp, _vp]
+_lib.rsa_decrypt_text.argtypes = [_vp, ctypes.c_size_t, _u32p, _u32p, ctypes.c_int, _vp, _vp, _vp]
 _lib.rsa_modexp_batch_paper.argtypes = [ctypes.c_void_p, ctypes.c_uint64, ctypes.c_uint32, ctypes.c_size_t,
                                         ctypes.c_void_p, ctypes.c_int, ctypes.c_void_p]
 
@@ -152,6 +154,36 @@ def rsa_decrypt_crt_batch(c, p: int, q: int, d: int, nbits: int, out=None, strea
         rc = _lib.rsa_decrypt_crt_batch(_vp(c.data_ptr()), _p(limbs(p, pl)), _p(limbs(q, pl)), pl, _p(limbs(d, s)),
                                         nbits, c.shape[0], _vp(out.data_ptr()), _vp(_stream_of(c, stream)))
     _check(rc, "rsa_decrypt_crt_batch")
+    return out
+
+
+def rsa_encrypt_text(text, e: int, n: int, nbits: int, status=None, stream=None):
+    """Fused sec. 2 codec + encryption.  text: CUDA uint8 tensor of lowercase
+    letters (spaces stripped, even length) or a str; returns [count, s]."""
+    import torch
+    if isinstance(text, str):
+        text = torch.tensor(list(text.replace(" ", "").encode("ascii")), dtype=torch.uint8, device="cuda")
+    s = nlimbs(nbits)
+    out = torch.empty((text.numel() // 2, s), dtype=torch.int32, device=text.device)
+    with torch.cuda.device(text.device):
+        rc = _lib.rsa_encrypt_text(_vp(text.data_ptr()), text.numel(), _p(limbs(e, s)), _p(limbs(n, s)), nbits,
+                                   _vp(out.data_ptr()), _vp(status.data_ptr() if status is not None else 0),
+                                   _vp(_stream_of(text, stream)))
+    _check(rc, "rsa_encrypt_text")
+    return out
+
+
+def rsa_decrypt_text(cipher, d: int, n: int, nbits: int, status=None, stream=None):
+    """Fused decryption + sec. 2 decoding; returns a CUDA uint8 tensor of letters."""
+    import torch
+    s = nlimbs(nbits)
+    cipher = cipher.contiguous()
+    out = torch.empty(2 * cipher.shape[0], dtype=torch.uint8, device=cipher.device)
+    with torch.cuda.device(cipher.device):
+        rc = _lib.rsa_decrypt_text(_vp(cipher.data_ptr()), cipher.shape[0], _p(limbs(d, s)), _p(limbs(n, s)), nbits,
+                                   _vp(out.data_ptr()), _vp(status.data_ptr() if status is not None else 0),
+                                   _vp(_stream_of(cipher, stream)))
+    _check(rc, "rsa_decrypt_text")
     return out
 
 

@@ -33,7 +33,12 @@ struct KCfg {
     static constexpr bool LOCKSTEP = (S >= 32);
 };
 
-template <int S>
+// IO = 0: limbs in, limbs out.  Codec modes (the
+// sec. 2 packetisation fused with the exponentiation, single-word moduli):
+// IO = 1: in = lowercase letters, two per packet, packet = hi*100 + lo
+// (PAPER.md:39-40); IO = 2: out = the two letters of each result packet.
+// Invalid letters / packets set status[i] (RSA_ECHAR = -7 / RSA_EPACKET = -10).
+template <int S, int IO = 0>
 __global__ void __launch_bounds__(KCfg<S>::BLOCK, KCfg<S>::MINB)
 modexp_kernel(const __grid_constant__ ModexpParams<S> p) {
     using V = typename BVec<S>::T;
@@ -54,9 +59,17 @@ modexp_kernel(const __grid_constant__ ModexpParams<S> p) {
         const bool valid = pkt0 < p.count;
         const unsigned long long pkt = valid ? pkt0 : p.count - 1;
         uint32_t a[S];
+        int io_status = 0;
         // a2: load the packet (packet-major at the boundary), zero padded
         const uint32_t* src = p.base + pkt * (unsigned long long)p.s_io;
-        if (p.s_io == S && (S % 4) == 0) {
+        if constexpr (IO == 1) {
+            const uchar2 ch = reinterpret_cast<const uchar2*>(p.base)[pkt];
+            const uint32_t hi = (uint32_t)ch.x - 'a', lo = (uint32_t)ch.y - 'a';
+            if (hi > 25u || lo > 25u) io_status = -7;
+#pragma unroll
+            for (int k = 0; k < S; k++) a[k] = 0u;
+            a[0] = (io_status ? 0u : hi * 100u + lo);
+        } else if (p.s_io == S && (S % 4) == 0) {
 #pragma unroll
             for (int k = 0; k < S; k += 4) {
                 const uint4 v = __ldg(reinterpret_cast<const uint4*>(src + k));
@@ -116,7 +129,22 @@ modexp_kernel(const __grid_constant__ ModexpParams<S> p) {
         }
 
         // a8: store the canonical result
-        if (valid) {
+        if constexpr (IO == 2) {
+            if (valid) {
+                bool high = false;
+#pragma unroll
+                for (int k = 1; k < S; k++) high = high || a[k] != 0u;
+                const uint32_t hi = a[0] / 100u, lo = a[0] % 100u;
+                uchar2 ch;
+                if (high || hi > 25u || lo > 25u) {
+                    io_status = -10;
+                    ch = make_uchar2('?', '?');
+                } else {
+                    ch = make_uchar2((unsigned char)('a' + hi), (unsigned char)('a' + lo));
+                }
+                reinterpret_cast<uchar2*>(p.out)[pkt] = ch;
+            }
+        } else if (valid) {
             uint32_t* dst = p.out + pkt * (unsigned long long)p.s_io;
             if (p.s_io == S && (S % 4) == 0) {
 #pragma unroll
@@ -127,6 +155,9 @@ modexp_kernel(const __grid_constant__ ModexpParams<S> p) {
                 for (int k = 0; k < S; k++)
                     if (k < p.s_io) dst[k] = a[k];
             }
+        }
+        if constexpr (IO != 0) {
+            if (valid && p.status) p.status[pkt] = io_status;
         }
     }
 }
@@ -299,7 +330,7 @@ __global__ void fill_one_kernel(uint32_t* out, unsigned long long count, int s_i
         out[i] = (i % s_io) == 0 ? 1u : 0u;
 }
 
-template <int S>
+template <int S, int IO = 0>
 static cudaError_t launch_class(const void* params, int sms, cudaStream_t stream, int* grid_out,
                                 int* block_out, size_t* tab_stride_out, bool query_only) {
     using V = typename BVec<S>::T;
@@ -307,10 +338,10 @@ static cudaError_t launch_class(const void* params, int sms, cudaStream_t stream
     const size_t smem = sizeof(V) * (S / BVec<S>::G) * block;
     static int occ = -1;
     if (occ < 0) {
-        cudaError_t e = cudaFuncSetAttribute(modexp_kernel<S>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        cudaError_t e = cudaFuncSetAttribute(modexp_kernel<S, IO>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              (int)smem);
         if (e != cudaSuccess) return e;
-        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, modexp_kernel<S>, block, smem);
+        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, modexp_kernel<S, IO>, block, smem);
         if (e != cudaSuccess) return e;
         if (occ < 1) occ = 1;
     }
@@ -319,7 +350,7 @@ static cudaError_t launch_class(const void* params, int sms, cudaStream_t stream
     if (block_out) *block_out = block;
     if (tab_stride_out) *tab_stride_out = (size_t)grid * block;
     if (query_only) return cudaSuccess;
-    modexp_kernel<S><<<grid, block, smem, stream>>>(*static_cast<const ModexpParams<S>*>(params));
+    modexp_kernel<S, IO><<<grid, block, smem, stream>>>(*static_cast<const ModexpParams<S>*>(params));
     return cudaGetLastError();
 }
 
@@ -341,6 +372,14 @@ cudaError_t rsa_b200_launch(int S, const void* params, int sms, cudaStream_t str
 }
 
 // per-packet table slots of the persistent grid for class S (threads, or
+// codec-fused launches (S = 2 class only): io = 1 text in, io = 2 text out
+cudaError_t rsa_b200_launch_codec(const void* params, int io, int sms, cudaStream_t stream) {
+    using namespace rsa_b200;
+    if (io == 1) return launch_class<2, 1>(params, sms, stream, nullptr, nullptr, nullptr, false);
+    if (io == 2) return launch_class<2, 2>(params, sms, stream, nullptr, nullptr, nullptr, false);
+    return cudaErrorInvalidValue;
+}
+
 // lane pairs for S = 128): sizes the table workspace
 cudaError_t rsa_b200_grid(int S, int sms, int* grid, int* block, size_t* nthreads) {
     using namespace rsa_b200;

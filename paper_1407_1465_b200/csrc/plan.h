@@ -39,8 +39,9 @@ struct __align__(8) RsaOp {
 // __grid_constant__ so n[] and r2[] are constant-bank operands of the IMADs.
 template <int S>
 struct ModexpParams {
-    const uint32_t* base;         // device, [count][s_io] LE limbs
-    uint32_t* out;                // device, [count][s_io]
+    const uint32_t* base;         // device, [count][s_io] LE limbs (or text bytes, codec mode)
+    uint32_t* out;                // device, [count][s_io] (or text bytes, codec mode)
+    int* status;                  // device, [count] per-packet codec status, or null
     void* table;                  // device workspace: ntab entries x S limbs x nthreads
     unsigned long long count;
     int s_io;                     // limbs per packet at the boundary (ceil(nbits/32))

@@ -22,6 +22,7 @@
 #include "plan.h"
 
 cudaError_t rsa_b200_launch(int S, const void* params, int sms, cudaStream_t stream);
+cudaError_t rsa_b200_launch_codec(const void* params, int io, int sms, cudaStream_t stream);
 cudaError_t rsa_b200_grid(int S, int sms, int* grid, int* block, size_t* nthreads);
 size_t rsa_b200_params_size(int S);
 cudaError_t rsa_b200_fill_one(uint32_t* out, unsigned long long count, int s_io, int sms, cudaStream_t stream);
@@ -166,6 +167,7 @@ static void fill_params(Plan& pl, const BN& n, const std::vector<RsaOp>& ops) {
 template <int S>
 static void patch_params(void* raw, const uint32_t* base, uint32_t* out, void* table, size_t count) {
     ModexpParams<S>* p = reinterpret_cast<ModexpParams<S>*>(raw);
+    p->status = nullptr;
     p->base = base;
     p->out = out;
     p->table = table;
@@ -284,6 +286,29 @@ static int check_modulus(const uint32_t* n, int nbits) {
     for (int i = 1; i < s && small; i++)
         if (n[i]) small = false;
     if (small) return RSA_EEVEN;
+    return RSA_OK;
+}
+
+// codec-fused batch (S = 2 class): io = 1 text -> ciphertext limbs, io = 2
+// limbs -> text; status may be null
+static int enqueue_codec(const Plan& pl, const void* in, void* out, size_t count, int io, int* status,
+                         cudaStream_t stream) {
+    const int sms = device_sms();
+    if (!sms || pl.S != 2) return RSA_ECUDA;
+    int grid = 0, block = 0;
+    size_t nthr = 0;
+    if (rsa_b200_grid(2, sms, &grid, &block, &nthr) != cudaSuccess) return RSA_ECUDA;
+    keep_pool_memory();
+    void* table = nullptr;
+    const size_t tbytes = (size_t)std::max(pl.ntab, 1) * 2 * sizeof(uint32_t) * nthr;
+    if (cudaMallocAsync(&table, tbytes, stream) != cudaSuccess) return RSA_ECUDA;
+    std::vector<unsigned char> params = pl.params;
+    patch_params<2>(params.data(), (const uint32_t*)in, (uint32_t*)out, table, count);
+    reinterpret_cast<ModexpParams<2>*>(params.data())->status = status;
+    cudaError_t e = rsa_b200_launch_codec(params.data(), io, sms, stream);
+    cudaFreeAsync(table, stream);
+    if (e != cudaSuccess) return RSA_ECUDA;
+    g_launches++;
     return RSA_OK;
 }
 
@@ -783,6 +808,43 @@ int rsa_decrypt_crt_batch(const uint32_t* c, const uint32_t* p, const uint32_t* 
     cudaFreeAsync(cp, cs);
     cudaFreeAsync(cq, cs);
     return rc;
+}
+
+
+// ------------------------------------------------------------------ f4: codec fused with the exponentiation
+
+int rsa_encrypt_text(const char* text, size_t nletters, const uint32_t* e, const uint32_t* n, int nbits,
+                     uint32_t* cipher, int* status, void* stream) {
+    if (!e || !n) return RSA_EINVAL;
+    if (nbits < 2 || nbits > 64) return RSA_ERANGE;
+    int st = check_modulus(n, nbits);
+    if (st) return st;
+    const int s = (nbits + 31) / 32;
+    uint64_t nv = n[0] | (s > 1 ? (uint64_t)n[1] << 32 : 0);
+    if (nv <= 2525) return RSA_ERANGE;                 // packets up to 2525 must be < n
+    if (nletters & 1) return RSA_EODD;
+    if (nletters == 0) return RSA_OK;
+    if (!text || !cipher) return RSA_EINVAL;
+    Plan pl;
+    st = get_plan(e, n, nbits, &pl);
+    if (st) return st;
+    if (pl.exp_zero) return RSA_EINVAL;
+    return enqueue_codec(pl, text, cipher, nletters / 2, 1, status, (cudaStream_t)stream);
+}
+
+int rsa_decrypt_text(const uint32_t* cipher, size_t count, const uint32_t* d, const uint32_t* n, int nbits,
+                     char* text, int* status, void* stream) {
+    if (!d || !n) return RSA_EINVAL;
+    if (nbits < 2 || nbits > 64) return RSA_ERANGE;
+    int st = check_modulus(n, nbits);
+    if (st) return st;
+    if (count == 0) return RSA_OK;
+    if (!text || !cipher) return RSA_EINVAL;
+    Plan pl;
+    st = get_plan(d, n, nbits, &pl);
+    if (st) return st;
+    if (pl.exp_zero) return RSA_EINVAL;
+    return enqueue_codec(pl, cipher, text, count, 2, status, (cudaStream_t)stream);
 }
 
 int rsa_set_window(int w) {
