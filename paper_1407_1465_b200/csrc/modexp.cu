@@ -15,9 +15,11 @@
 // the batch), so control flow is warp-uniform: no divergence.
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <stdlib.h>
 
 #include "mont.cuh"
 #include "mont_pair.cuh"
+#include "mont_group.cuh"
 #include "mont_sqr.cuh"
 #include "plan.h"
 
@@ -322,6 +324,132 @@ __global__ void paper_fig12_kernel(const uint32_t* __restrict__ num, uint64_t ke
     result[i] = (uint32_t)ret;
 }
 
+
+// ---------------------------------------------------------------------------
+// S = TPI * L limbs with TPI lanes per packet (mont_group.cuh): the 4096-bit
+// class runs TPI = 4 (L = 32, ~2x the resident warps of the lane-pair shape).
+template <int S, int TPI>
+__global__ void __launch_bounds__(128, (TPI >= 4) ? 3 : 2)
+modexp_group_kernel(const __grid_constant__ ModexpParams<S> p) {
+    constexpr int L = S / TPI;
+    constexpr int NG = S / 4;         // uint4 groups per packet
+    constexpr int NGL = L / 4;        // groups per lane
+    constexpr int NQ = L / 8;         // uint4 of odd (even) limbs per lane
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    uint4* const nodd_all = reinterpret_cast<uint4*>(smem_raw);
+    uint4* const neven_all = nodd_all + TPI * NQ;
+    uint4* const slots = neven_all + TPI * NQ;
+    const int ppb = blockDim.x / TPI;
+    for (int i = threadIdx.x; i < TPI * NQ; i += blockDim.x) {
+        const int h = i / NQ, q = i % NQ, o = h * L + 8 * q;
+        nodd_all[i] = make_uint4(p.n[o + 1], p.n[o + 3], p.n[o + 5], p.n[o + 7]);
+        neven_all[i] = make_uint4(p.n[o], p.n[o + 2], p.n[o + 4], p.n[o + 6]);
+    }
+    __syncthreads();
+    const int lig = threadIdx.x & (TPI - 1);
+    const int pk = threadIdx.x / TPI;
+    const uint4* nodd4 = nodd_all + lig * NQ;
+    const uint4* neven4 = neven_all + lig * NQ;
+    uint4* const bslot = slots + pk;
+    const unsigned gpk = (blockIdx.x * blockDim.x + threadIdx.x) / TPI;
+    const unsigned npk = (gridDim.x * blockDim.x) / TPI;
+    uint4* const table = reinterpret_cast<uint4*>(p.table);
+    const unsigned long long trips = (p.count + npk - 1) / npk;
+
+    for (unsigned long long t = 0; t < trips; t++) {
+        const unsigned long long pkt0 = gpk + t * npk;
+        const bool valid = pkt0 < p.count;
+        const unsigned long long pkt = valid ? pkt0 : p.count - 1;
+        uint32_t a[L];
+        const uint32_t* src = p.base + pkt * (unsigned long long)p.s_io;
+        if (p.s_io == S) {
+#pragma unroll
+            for (int k = 0; k < L; k += 4) {
+                const uint4 v = __ldg(reinterpret_cast<const uint4*>(src + lig * L + k));
+                a[k] = v.x; a[k + 1] = v.y; a[k + 2] = v.z; a[k + 3] = v.w;
+            }
+        } else {
+#pragma unroll
+            for (int k = 0; k < L; k++) a[k] = (lig * L + k < p.s_io) ? __ldg(src + lig * L + k) : 0u;
+        }
+        for (int i = 0; i < p.nops; i++) {
+            const RsaOp op = p.ops[i];
+            if (op.flags & RSA_F_LOADA) {
+#pragma unroll
+                for (int g = 0; g < NGL; g++) {
+                    const uint4 v = table[((size_t)op.lidx * NG + lig * NGL + g) * npk + gpk];
+                    a[4 * g] = v.x; a[4 * g + 1] = v.y; a[4 * g + 2] = v.z; a[4 * g + 3] = v.w;
+                }
+            }
+            for (int r = 0; r < op.rep; r++) {
+                __syncwarp();
+                if (op.kind == RSA_OP_SQR) {
+#pragma unroll
+                    for (int g = 0; g < NGL; g++)
+                        bslot[(lig * NGL + g) * ppb] = make_uint4(a[4 * g], a[4 * g + 1], a[4 * g + 2], a[4 * g + 3]);
+                } else if (op.kind == RSA_OP_MUL) {
+#pragma unroll
+                    for (int g = 0; g < NGL; g++)
+                        bslot[(lig * NGL + g) * ppb] = table[((size_t)op.bidx * NG + lig * NGL + g) * npk + gpk];
+                } else if (op.kind == RSA_OP_R2) {
+#pragma unroll
+                    for (int g = 0; g < NGL; g++) {
+                        const int o = lig * L + 4 * g;
+                        bslot[(lig * NGL + g) * ppb] = make_uint4(p.r2[o], p.r2[o + 1], p.r2[o + 2], p.r2[o + 3]);
+                    }
+                } else {
+#pragma unroll
+                    for (int g = 0; g < NGL; g++)
+                        bslot[(lig * NGL + g) * ppb] = make_uint4((lig == 0 && g == 0) ? 1u : 0u, 0u, 0u, 0u);
+                }
+                __syncwarp();
+                montmul_group<L, TPI>(a, bslot, ppb, nodd4, neven4, p.n0inv, lig);
+            }
+            if (op.flags & RSA_F_STORE) {
+#pragma unroll
+                for (int g = 0; g < NGL; g++)
+                    table[((size_t)op.sidx * NG + lig * NGL + g) * npk + gpk] =
+                        make_uint4(a[4 * g], a[4 * g + 1], a[4 * g + 2], a[4 * g + 3]);
+            }
+        }
+        if (valid) {
+            uint32_t* dst = p.out + pkt * (unsigned long long)p.s_io;
+            if (p.s_io == S) {
+#pragma unroll
+                for (int k = 0; k < L; k += 4)
+                    *reinterpret_cast<uint4*>(dst + lig * L + k) = make_uint4(a[k], a[k + 1], a[k + 2], a[k + 3]);
+            } else {
+#pragma unroll
+                for (int k = 0; k < L; k++)
+                    if (lig * L + k < p.s_io) dst[lig * L + k] = a[k];
+            }
+        }
+    }
+}
+
+template <int S, int TPI>
+static cudaError_t launch_group(const void* params, int sms, cudaStream_t stream, int* grid_out,
+                                int* block_out, size_t* slots_out, bool query_only) {
+    const int block = 128;
+    const size_t smem = sizeof(uint4) * (2 * TPI * (S / TPI / 8) + (S / 4) * (block / TPI));
+    static int occ = -1;
+    if (occ < 0) {
+        cudaError_t e = cudaFuncSetAttribute(modexp_group_kernel<S, TPI>,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return e;
+        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, modexp_group_kernel<S, TPI>, block, smem);
+        if (e != cudaSuccess) return e;
+        if (occ < 1) occ = 1;
+    }
+    const int grid = sms * occ;
+    if (grid_out) *grid_out = grid;
+    if (block_out) *block_out = block;
+    if (slots_out) *slots_out = (size_t)grid * block / TPI;
+    if (query_only) return cudaSuccess;
+    modexp_group_kernel<S, TPI><<<grid, block, smem, stream>>>(*static_cast<const ModexpParams<S>*>(params));
+    return cudaGetLastError();
+}
+
 // exp == 0: every output is 1 mod n = 1 (n >= 3), reading Z12
 __global__ void fill_one_kernel(uint32_t* out, unsigned long long count, int s_io) {
     const unsigned long long total = count * (unsigned long long)s_io;
@@ -356,6 +484,29 @@ static cudaError_t launch_class(const void* params, int sms, cudaStream_t stream
 
 }  // namespace rsa_b200
 
+// Lanes per packet for the 4096-bit class: 2 (default, mont_pair.cuh) or 4
+// (mont_group.cuh), selectable with RSA_B200_TPI128 for measurement
+// (B200: 47.9K vs 45.6K RSA-4096 full-d decrypts/s, profiles/r01_shape_ab.json).
+// Shape of the 2048-bit class: thread per packet (default) or a 2-lane group
+// (RSA_B200_SHAPE64=group2), for the measured choice recorded in DESIGN.md.
+static int rsa_b200_shape64() {
+    static int v = -1;
+    if (v < 0) {
+        const char* e = getenv("RSA_B200_SHAPE64");
+        v = (e && e[0] == 'g') ? 1 : 0;
+    }
+    return v;
+}
+
+static int rsa_b200_tpi128() {
+    static int v = 0;
+    if (!v) {
+        const char* e = getenv("RSA_B200_TPI128");
+        v = (e && e[0] == '4') ? 4 : 2;
+    }
+    return v;
+}
+
 // Host entry points used by rsa_abi.cpp (C++ linkage, not part of the C-ABI).
 cudaError_t rsa_b200_launch(int S, const void* params, int sms, cudaStream_t stream) {
     using namespace rsa_b200;
@@ -365,8 +516,10 @@ cudaError_t rsa_b200_launch(int S, const void* params, int sms, cudaStream_t str
     case 8: return launch_class<8>(params, sms, stream, nullptr, nullptr, nullptr, false);
     case 16: return launch_class<16>(params, sms, stream, nullptr, nullptr, nullptr, false);
     case 32: return launch_class<32>(params, sms, stream, nullptr, nullptr, nullptr, false);
-    case 64: return launch_class<64>(params, sms, stream, nullptr, nullptr, nullptr, false);
-    case 128: return launch_pair<128>(params, sms, stream, nullptr, nullptr, nullptr, false);
+    case 64: return rsa_b200_shape64() ? launch_group<64, 2>(params, sms, stream, nullptr, nullptr, nullptr, false)
+                                       : launch_class<64>(params, sms, stream, nullptr, nullptr, nullptr, false);
+    case 128: return rsa_b200_tpi128() == 2 ? launch_pair<128>(params, sms, stream, nullptr, nullptr, nullptr, false)
+                                            : launch_group<128, 4>(params, sms, stream, nullptr, nullptr, nullptr, false);
     default: return cudaErrorInvalidValue;
     }
 }
@@ -389,8 +542,10 @@ cudaError_t rsa_b200_grid(int S, int sms, int* grid, int* block, size_t* nthread
     case 8: return launch_class<8>(nullptr, sms, 0, grid, block, nthreads, true);
     case 16: return launch_class<16>(nullptr, sms, 0, grid, block, nthreads, true);
     case 32: return launch_class<32>(nullptr, sms, 0, grid, block, nthreads, true);
-    case 64: return launch_class<64>(nullptr, sms, 0, grid, block, nthreads, true);
-    case 128: return launch_pair<128>(nullptr, sms, 0, grid, block, nthreads, true);
+    case 64: return rsa_b200_shape64() ? launch_group<64, 2>(nullptr, sms, 0, grid, block, nthreads, true)
+                                       : launch_class<64>(nullptr, sms, 0, grid, block, nthreads, true);
+    case 128: return rsa_b200_tpi128() == 2 ? launch_pair<128>(nullptr, sms, 0, grid, block, nthreads, true)
+                                            : launch_group<128, 4>(nullptr, sms, 0, grid, block, nthreads, true);
     default: return cudaErrorInvalidValue;
     }
 }

@@ -1,0 +1,39 @@
+"""The alternative kernel shapes kept for measurement ('chosen by
+measurement'): 2048-bit as a 2-lane group (RSA_B200_SHAPE64=group2) and
+4096-bit as a 4-lane group (RSA_B200_TPI128=4) stay bit-exact vs the oracle.
+Run in subprocesses (the switch is read once per process)."""
+import os
+import subprocess
+import sys
+
+import pytest
+
+pytestmark = pytest.mark.gpu
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+SCRIPT = r'''
+import sys, numpy as np, torch
+sys.path.insert(0, %r)
+import oracle, workload, paper_1407_1465_b200 as R
+k = workload.key(sys.argv[1]); nb = k["nbits"]; s = workload.limbs_needed(nb)
+m = workload.packets(int(sys.argv[2]), nb, n=k["n"], config_id=21)
+t = torch.from_numpy(m.view(np.int32)).cuda()
+for e in (k["e"], k["d"]):
+    got = R.rsa_modexp_batch(t, e, k["n"], nb).cpu().numpy().view(np.uint32)
+    assert np.array_equal(got, oracle.modexp_batch(m, e, k["n"])[:, :s]), e
+print("shape ok")
+''' % ROOT
+
+
+@pytest.mark.parametrize("env,key,count", [("RSA_B200_SHAPE64=group2", "rsa2048", 300),
+                                           ("RSA_B200_SHAPE64=group2", "rsa1536", 300),
+                                           ("RSA_B200_TPI128=4", "rsa4096", 60),
+                                           ("RSA_B200_TPI128=4", "rsa3072", 60)])
+def test_alternative_shapes(env, key, count):
+    torch = pytest.importorskip("torch")
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    k, v = env.split("=")
+    r = subprocess.run([sys.executable, "-c", SCRIPT, key, str(count)], capture_output=True, text=True,
+                       timeout=900, env=dict(os.environ, **{k: v}))
+    assert r.returncode == 0 and "shape ok" in r.stdout, (r.stdout + r.stderr)[-2000:]
