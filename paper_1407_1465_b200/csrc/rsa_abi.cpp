@@ -312,8 +312,19 @@ static int enqueue_codec(const Plan& pl, const void* in, void* out, size_t count
     return RSA_OK;
 }
 
-// enqueue one batch on `stream` (device pointers, validated arguments)
-static int enqueue(const Plan& pl, const uint32_t* base, uint32_t* out, size_t count, cudaStream_t stream) {
+// window-table workspace bytes of a plan on the current device
+static size_t table_bytes(const Plan& pl) {
+    const int sms = device_sms();
+    int grid = 0, block = 0;
+    size_t nthr = 0;
+    if (!sms || pl.exp_zero || rsa_b200_grid(pl.S, sms, &grid, &block, &nthr) != cudaSuccess) return 0;
+    return (size_t)pl.ntab * pl.S * sizeof(uint32_t) * nthr;
+}
+
+// enqueue one batch on `stream` (device pointers, validated arguments).  If
+// `table` is null the workspace is allocated stream-ordered for this launch.
+static int enqueue(const Plan& pl, const uint32_t* base, uint32_t* out, size_t count, cudaStream_t stream,
+                   void* table = nullptr) {
     const int sms = device_sms();
     if (!sms) return RSA_ECUDA;
     if (pl.exp_zero) {
@@ -321,17 +332,15 @@ static int enqueue(const Plan& pl, const uint32_t* base, uint32_t* out, size_t c
         g_launches++;
         return RSA_OK;
     }
-    int grid = 0, block = 0;
-    size_t nthr = 0;
-    if (rsa_b200_grid(pl.S, sms, &grid, &block, &nthr) != cudaSuccess) return RSA_ECUDA;
-    keep_pool_memory();
-    void* table = nullptr;
-    const size_t tbytes = (size_t)pl.ntab * pl.S * sizeof(uint32_t) * nthr;
-    if (cudaMallocAsync(&table, tbytes, stream) != cudaSuccess) return RSA_ECUDA;
+    const bool own = (table == nullptr);
+    if (own) {
+        keep_pool_memory();
+        if (cudaMallocAsync(&table, table_bytes(pl), stream) != cudaSuccess) return RSA_ECUDA;
+    }
     std::vector<unsigned char> params = pl.params;
     patch(pl.S, params.data(), base, out, table, count);
     cudaError_t e = rsa_b200_launch(pl.S, params.data(), sms, stream);
-    cudaFreeAsync(table, stream);
+    if (own) cudaFreeAsync(table, stream);
     if (e != cudaSuccess) return RSA_ECUDA;
     g_launches++;
     return RSA_OK;
@@ -523,9 +532,13 @@ int rsa_modexp_batch_host(const uint32_t* base_host, const uint32_t* exp, const 
     }
     keep_pool_memory();
     uint32_t* dbuf[2] = {nullptr, nullptr};
+    void* tab[2] = {nullptr, nullptr};
+    const size_t tb = table_bytes(pl);
     int rc = RSA_OK;
-    for (int k = 0; k < 2 && rc == RSA_OK; k++)
+    for (int k = 0; k < 2 && rc == RSA_OK; k++) {
         if (cudaMallocAsync((void**)&dbuf[k], per * row, ss[k]) != cudaSuccess) rc = RSA_ECUDA;
+        if (tb && rc == RSA_OK && cudaMallocAsync(&tab[k], tb, ss[k]) != cudaSuccess) rc = RSA_ECUDA;
+    }
     for (size_t c = 0; c < nch && rc == RSA_OK; c++) {
         const size_t lo = c * per;
         if (lo >= count) break;
@@ -536,13 +549,14 @@ int rsa_modexp_batch_host(const uint32_t* base_host, const uint32_t* exp, const 
             rc = RSA_ECUDA;
             break;
         }
-        rc = enqueue(pl, d, d, cnt, sc);
+        rc = enqueue(pl, d, d, cnt, sc, tab[c & 1]);
         if (rc) break;
         if (cudaMemcpyAsync(out_host + lo * s, d, cnt * row, cudaMemcpyDeviceToHost, sc) != cudaSuccess)
             rc = RSA_ECUDA;
     }
     for (int k = 0; k < 2; k++) {
         if (dbuf[k]) cudaFreeAsync(dbuf[k], ss[k]);
+        if (tab[k]) cudaFreeAsync(tab[k], ss[k]);
         if (cudaStreamSynchronize(ss[k]) != cudaSuccess) rc = RSA_ECUDA;
         cudaStreamDestroy(ss[k]);
     }
