@@ -61,6 +61,8 @@ def parse():
     ap.add_argument("--config", default="rsa2048-roundtrip", choices=sorted(WORKLOADS))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--count", type=int, default=0, help="override packets per rank (profiling only)")
+    ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
+                    help="process-group backend for N > 1 (gloo: test the multi-rank path on fewer GPUs)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=20.0, help="CPU-seconds budget of the oracle sample")
@@ -323,7 +325,8 @@ def run_ours(args, rank, world, local_rank):
     leg_ms = [statistics.mean(leg_events[k][j][0].elapsed_time(leg_events[k][j][1]) for k in range(args.steps))
               for j in range(len(legs))]
     if world > 1:
-        t = torch.tensor([elapsed_ms] + leg_ms, device=dev, dtype=torch.float64)
+        on_dev = dist.get_backend() == "nccl"
+        t = torch.tensor([elapsed_ms] + leg_ms, device=dev if on_dev else "cpu", dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         elapsed_ms, leg_ms = float(t[0]), [float(v) for v in t[1:]]
 
@@ -417,8 +420,14 @@ def main():
     if world > 1:
         import torch
         import torch.distributed as dist
-        torch.cuda.set_device(local_rank)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        if args.dist_backend == "nccl":
+            torch.cuda.set_device(local_rank)
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        else:
+            # ranks share the visible devices round-robin (testing the N > 1 path)
+            local_rank = local_rank % max(1, torch.cuda.device_count())
+            torch.cuda.set_device(local_rank)
+            dist.init_process_group("gloo")
     try:
         run_ours(args, rank, world, local_rank)
     finally:
