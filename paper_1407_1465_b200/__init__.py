@@ -35,7 +35,7 @@ EXPORTS = ["rsa_strerror", "rsa_keygen_check", "rsa_validate_key", "rsa_modexp_b
            "rsa_decrypt_crt_batch", "rsa_encrypt_text", "rsa_decrypt_text"]
 
 if not os.path.exists(LIB_PATH):
-    raise ImportError(f"{LIB_PATH} is not built: run `python -m paper_1407_1465_b200.build` "
+    raise ImportError(f"{LIB_PATH} is not built: run `python paper_1407_1465_b200/build.py` "
                       "(no CPU fallback exists)")
 
 _lib = ctypes.CDLL(LIB_PATH)
