@@ -29,11 +29,12 @@ def build(force: bool = False, verbose: bool = False) -> str:
            "-Xptxas", "-v" if verbose else "-O3", "-o", LIB + ".tmp", *SOURCES]
     subprocess.check_call(cmd)
     os.replace(LIB + ".tmp", LIB)
-    # the microbenchmark executable (roofline denominator), built alongside
-    mb = os.path.join(CSRC, "microbench", "imad_peak")
-    src = mb + ".cu"
-    if os.path.exists(src) and (force or not os.path.exists(mb) or os.path.getmtime(mb) < os.path.getmtime(src)):
-        subprocess.check_call([NVCC, *ARCH, "-O3", "-lineinfo", "-o", mb, src])
+    # the microbenchmarks (roofline denominator, chain latency), built alongside
+    for name in ("imad_peak", "imad_latency"):
+        mb = os.path.join(CSRC, "microbench", name)
+        src = mb + ".cu"
+        if os.path.exists(src) and (force or not os.path.exists(mb) or os.path.getmtime(mb) < os.path.getmtime(src)):
+            subprocess.check_call([NVCC, *ARCH, "-O3", "-lineinfo", "-o", mb, src])
     return LIB
 
 

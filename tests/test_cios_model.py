@@ -308,3 +308,39 @@ def test_montsqr_model(S):
     for N, A in cases:
         got = montsqr_model(L(A, S), L(N, S), S)
         assert got == (A * A * pow(R, -1, N)) % N
+
+
+# ---------------------------------------------------------------- v2 squaring: fused doubling + diagonal
+
+def square_fused_columns(a, S):
+    """Column loop of mont_v2.cuh: per column, fresh off-diagonal accumulators
+    (two interleaved), doubled, + diagonal, + the running 2-word carry."""
+    T = [0] * (2 * S)
+    r0 = r1 = 0
+    for k in range(2 * S):
+        lo, top = max(0, k - S + 1), (k - 1) // 2
+        c = [0, 0, 0]
+        d = [0, 0, 0]
+        for i in range(lo, top + 1):
+            acc = c if (i - lo) % 2 == 0 else d
+            v = acc[0] + (acc[1] << 32) + (acc[2] << 64) + a[i] * a[k - i]
+            acc[0], acc[1], acc[2] = v & M32, (v >> 32) & M32, v >> 64
+        v = c[0] + (c[1] << 32) + (c[2] << 64) + d[0] + (d[1] << 32) + (d[2] << 64)
+        v = 2 * v
+        if k % 2 == 0 and k // 2 < S:
+            v += a[k // 2] * a[k // 2]
+        v += r0 + (r1 << 32)
+        assert v < 1 << 96
+        T[k] = v & M32
+        r0, r1 = (v >> 32) & M32, v >> 64
+        assert r1 < 2**32
+    assert r0 == 0 and r1 == 0
+    return T
+
+
+@pytest.mark.parametrize("S", [2, 4, 8, 64])
+def test_square_fused_columns(S):
+    rnd = random.Random(300 + S)
+    for A in [0, 1, (1 << (32 * S)) - 1] + [rnd.getrandbits(32 * S) for _ in range(50)]:
+        T = square_fused_columns(L(A, S), S)
+        assert sum(v << (32 * k) for k, v in enumerate(T)) == A * A
