@@ -168,10 +168,25 @@ modexp_multi_kernel(const __grid_constant__ MultiParams p) {
         constexpr int K = (S == 8) ? 8 : (S == 16) ? 9 : (S == 32) ? 10 : 11;
         const int s_tab = K + 1, s_scan = K + 1 + (nent - 2);
         const int s_fin = s_scan + (nwin - 1) * (w + 1);
-        const int total = s_fin + (p.mode == 0 ? 1 : eoff - 1);
+        // lockstep (S >= 64): a barrier per step keeps the CTA's warps on the
+        // same code lines; the Miller-Rabin tail runs to the block's largest r
+        // (extra squarings of a thread past its own r do not change its verdict)
+        int tail = (p.mode == 0 ? 1 : eoff - 1);
+        if constexpr (S >= 64) {
+            __shared__ int s_tail;
+            if (threadIdx.x == 0) s_tail = 0;
+            __syncthreads();
+            atomicMax(&s_tail, tail);
+            __syncthreads();
+            tail = s_tail;
+            __syncthreads();
+        }
+        const int total = s_fin + tail;
+        const int my_total = s_fin + (p.mode == 0 ? 1 : eoff - 1);
         uint32_t mone[S];
         bool prime = false;
         for (int st = 0; st < total; st++) {
+            if constexpr (S >= 64) __syncthreads();
             bool sqr;
             if (st < K) {
                 sqr = true;
@@ -231,14 +246,14 @@ modexp_multi_kernel(const __grid_constant__ MultiParams p) {
             if (sqr) montsqr_sm<S>(a, nsh, n0inv);
             else montmul_sm<S>(a, bslot, stride, nsh, n0inv);
             if (st >= K && st < s_scan) store_a(st - K + 1, a);   // T[1] .. T[nent-1]
-            if (p.mode == 1 && st >= s_fin) {
+            if (p.mode == 1 && st >= s_fin && st < my_total) {
                 bool e = true;
 #pragma unroll
                 for (int k = 0; k < S; k++) e = e && a[k] == mone[k];
                 prime = prime || e;
             }
         }
-        if (p.mode == 1 && total == s_fin) {                 // r == 1: no squaring after the scan
+        if (p.mode == 1 && my_total == s_fin && total == s_fin) {   // r == 1 everywhere: no squaring after the scan
             if (s_fin == s_scan) load_a((int)exp_bits_at(esrc, p.s_io, eoff, ebits), a);
             uint32_t one[S];
             load_a(0, one);
