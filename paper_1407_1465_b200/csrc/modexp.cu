@@ -283,12 +283,15 @@ static cudaError_t launch_pair(const void* params, int sms, cudaStream_t stream,
         if (e != cudaSuccess) return e;
         if (occ < 1) occ = 1;
     }
-    const int grid = sms * occ;
+    int grid = sms * occ;
     if (grid_out) *grid_out = grid;
     if (block_out) *block_out = block;
     if (slots_out) *slots_out = (size_t)grid * block / 2;
     if (query_only) return cudaSuccess;
-    modexp_pair_kernel<S><<<grid, block, smem, stream>>>(*static_cast<const ModexpParams<S>*>(params));
+    const ModexpParams<S>& prm = *static_cast<const ModexpParams<S>*>(params);
+    const unsigned long long need = (prm.count + block / 2 - 1) / (block / 2);
+    if (need < (unsigned long long)grid) grid = (int)need;
+    modexp_pair_kernel<S><<<grid, block, smem, stream>>>(prm);
     return cudaGetLastError();
 }
 
@@ -441,12 +444,15 @@ static cudaError_t launch_group(const void* params, int sms, cudaStream_t stream
         if (e != cudaSuccess) return e;
         if (occ < 1) occ = 1;
     }
-    const int grid = sms * occ;
+    int grid = sms * occ;
     if (grid_out) *grid_out = grid;
     if (block_out) *block_out = block;
     if (slots_out) *slots_out = (size_t)grid * block / TPI;
     if (query_only) return cudaSuccess;
-    modexp_group_kernel<S, TPI><<<grid, block, smem, stream>>>(*static_cast<const ModexpParams<S>*>(params));
+    const ModexpParams<S>& prm = *static_cast<const ModexpParams<S>*>(params);
+    const unsigned long long need = (prm.count + block / TPI - 1) / (block / TPI);
+    if (need < (unsigned long long)grid) grid = (int)need;
+    modexp_group_kernel<S, TPI><<<grid, block, smem, stream>>>(prm);
     return cudaGetLastError();
 }
 
@@ -473,12 +479,17 @@ static cudaError_t launch_class(const void* params, int sms, cudaStream_t stream
         if (e != cudaSuccess) return e;
         if (occ < 1) occ = 1;
     }
-    const int grid = sms * occ;
+    int grid = sms * occ;
     if (grid_out) *grid_out = grid;
     if (block_out) *block_out = block;
     if (tab_stride_out) *tab_stride_out = (size_t)grid * block;
     if (query_only) return cudaSuccess;
-    modexp_kernel<S, IO><<<grid, block, smem, stream>>>(*static_cast<const ModexpParams<S>*>(params));
+    // small batches: no more CTAs than packets need (latency; the workspace
+    // sized for the full grid is indexed by the actual thread count)
+    const ModexpParams<S>& prm = *static_cast<const ModexpParams<S>*>(params);
+    const unsigned long long need = (prm.count + block - 1) / block;
+    if (need < (unsigned long long)grid) grid = (int)need;
+    modexp_kernel<S, IO><<<grid, block, smem, stream>>>(prm);
     return cudaGetLastError();
 }
 

@@ -13,6 +13,7 @@
 #include <algorithm>
 #include <atomic>
 #include <map>
+#include <memory>
 #include <mutex>
 #include <string>
 #include <vector>
@@ -187,9 +188,18 @@ static void patch(int S, void* raw, const uint32_t* base, uint32_t* out, void* t
 }
 
 static std::mutex g_plan_mu;
-static std::map<std::string, Plan> g_plans;
+static std::map<std::string, std::shared_ptr<const Plan>> g_plans;
+
+static int get_plan_ptr(const uint32_t* exp, const uint32_t* n, int nbits, std::shared_ptr<const Plan>* outp);
 
 static int get_plan(const uint32_t* exp, const uint32_t* n, int nbits, Plan* out) {
+    std::shared_ptr<const Plan> pp;
+    const int st = get_plan_ptr(exp, n, nbits, &pp);
+    if (st == RSA_OK) *out = *pp;
+    return st;
+}
+
+static int get_plan_ptr(const uint32_t* exp, const uint32_t* n, int nbits, std::shared_ptr<const Plan>* outp) {
     const int s_io = (nbits + 31) / 32;
     const int wov = t_window_override;
     std::string key((const char*)&nbits, sizeof(int));
@@ -200,7 +210,7 @@ static int get_plan(const uint32_t* exp, const uint32_t* n, int nbits, Plan* out
         std::lock_guard<std::mutex> lk(g_plan_mu);
         auto it = g_plans.find(key);
         if (it != g_plans.end()) {
-            *out = it->second;
+            *outp = it->second;
             return RSA_OK;
         }
     }
@@ -248,19 +258,23 @@ static int get_plan(const uint32_t* exp, const uint32_t* n, int nbits, Plan* out
         case 128: fill_params<128>(pl, N, best_ops); break;
         }
     }
+    auto sp = std::make_shared<const Plan>(std::move(pl));
     {
         std::lock_guard<std::mutex> lk(g_plan_mu);
         if (g_plans.size() > 256) g_plans.clear();
-        g_plans[key] = pl;
+        g_plans[key] = sp;
     }
-    *out = pl;
+    *outp = sp;
     return RSA_OK;
 }
 
 static int device_sms() {
+    static std::atomic<int> cache[64];
     int dev = 0, sms = 0;
     if (cudaGetDevice(&dev) != cudaSuccess) return 0;
+    if (dev >= 0 && dev < 64 && (sms = cache[dev].load()) > 0) return sms;
     if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) return 0;
+    if (dev >= 0 && dev < 64) cache[dev].store(sms);
     return sms;
 }
 
@@ -490,10 +504,10 @@ int rsa_modexp_batch(const uint32_t* base, const uint32_t* exp, const uint32_t* 
     const char* b0 = (const char*)base;
     const char* o0 = (const char*)out;
     if (b0 != o0 && b0 < o0 + bytes && o0 < b0 + bytes) return RSA_EINVAL;   // partial overlap
-    Plan pl;
-    st = get_plan(exp, n, nbits, &pl);
+    std::shared_ptr<const Plan> pl;
+    st = get_plan_ptr(exp, n, nbits, &pl);
     if (st) return st;
-    return enqueue(pl, base, out, count, (cudaStream_t)stream);
+    return enqueue(*pl, base, out, count, (cudaStream_t)stream);
 }
 
 int rsa_modexp_batch_host(const uint32_t* base_host, const uint32_t* exp, const uint32_t* n, int nbits,
