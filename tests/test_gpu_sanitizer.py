@@ -1,6 +1,6 @@
 """compute-sanitizer over every kernel (race detection):
 memcheck, racecheck (shared-memory hazards), initcheck, synccheck on tiny
-inputs (tools/sanitize_run.py, oracle-checked)."""
+inputs (tests/tools/sanitize_run.py, oracle-checked)."""
 import os
 import shutil
 import subprocess
@@ -23,7 +23,7 @@ def test_compute_sanitizer(tool):
     env = dict(os.environ, SAN_COUNT="40", PYTORCH_NO_CUDA_MEMORY_CACHING="1")
     extra = []
     r = subprocess.run([cs, "--tool", tool, "--error-exitcode", "99", "--target-processes", "all", *extra,
-                        sys.executable, os.path.join(ROOT, "tools", "sanitize_run.py")],
+                        sys.executable, os.path.join(ROOT, "tests", "tools", "sanitize_run.py")],
                        capture_output=True, text=True, timeout=900, env=env)
     tail = (r.stdout + r.stderr)[-3000:]
     assert r.returncode == 0, tail

@@ -6,7 +6,7 @@ inputs (values 0..800), device time by CUDA events (median of
 20 runs, the paper averaged 20).  Context only: the paper's
 seconds were GT 630M wall clock including transfers.
 
-    python tools/paper_tables.py > profiles/r01_paper_tables.json
+    python tests/tools/paper_tables.py > profiles/r01_paper_tables.json
 """
 import json
 import os
@@ -16,7 +16,7 @@ import sys
 import numpy as np
 import torch
 
-sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)))))
 import oracle  # noqa: E402  (checker only)
 import paper_1407_1465_b200 as R  # noqa: E402
 import workload  # noqa: E402
