@@ -67,7 +67,10 @@ modexp_multi_kernel(const __grid_constant__ MultiParams p) {
     const int w = p.window;
     const int nent = 1 << w;
     const unsigned long long trips = (p.count + nthr - 1) / nthr;
-    auto tab = [&](int entry, int g) -> uint4& { return p.table[((size_t)entry * NG + g) * nthr + gtid]; };
+    // per-thread contiguous entries: with per-packet exponents the lanes of a
+    // warp read different entries, so each entry is one thread's 16*S bytes
+    // (whole lines) rather than striped across threads
+    auto tab = [&](int entry, int g) -> uint4& { return p.table[((size_t)gtid * nent + entry) * NG + g]; };
     auto store_a = [&](int entry, const uint32_t (&v)[S]) {
 #pragma unroll
         for (int g = 0; g < NG; g++) tab(entry, g) = make_uint4(v[4 * g], v[4 * g + 1], v[4 * g + 2], v[4 * g + 3]);
