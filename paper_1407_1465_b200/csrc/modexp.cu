@@ -561,18 +561,6 @@ cudaError_t rsa_b200_grid(int S, int sms, int* grid, int* block, size_t* nthread
     }
 }
 
-size_t rsa_b200_params_size(int S) {
-    using namespace rsa_b200;
-    switch (S) {
-    case 2: return sizeof(ModexpParams<2>);
-    case 4: return sizeof(ModexpParams<4>);
-    case 8: return sizeof(ModexpParams<8>);
-    case 16: return sizeof(ModexpParams<16>);
-    case 32: return sizeof(ModexpParams<32>);
-    case 64: return sizeof(ModexpParams<64>);
-    case 128: return sizeof(ModexpParams<128>);
-    default: return 0;
-    }
 }
 
 cudaError_t rsa_b200_fill_one(uint32_t* out, unsigned long long count, int s_io, int sms, cudaStream_t stream) {

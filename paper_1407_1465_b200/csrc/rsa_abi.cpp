@@ -25,7 +25,6 @@
 cudaError_t rsa_b200_launch(int S, const void* params, int sms, cudaStream_t stream);
 cudaError_t rsa_b200_launch_codec(const void* params, int io, int sms, cudaStream_t stream);
 cudaError_t rsa_b200_grid(int S, int sms, int* grid, int* block, size_t* nthreads);
-size_t rsa_b200_params_size(int S);
 cudaError_t rsa_b200_fill_one(uint32_t* out, unsigned long long count, int s_io, int sms, cudaStream_t stream);
 cudaError_t rsa_b200_multi(int S, const uint32_t* base, const uint32_t* exps, const uint32_t* mods, uint32_t* out,
                            int32_t* status, void* table, unsigned long long count, int s_io, int exp_bits,
