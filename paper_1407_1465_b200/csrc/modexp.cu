@@ -561,8 +561,6 @@ cudaError_t rsa_b200_grid(int S, int sms, int* grid, int* block, size_t* nthread
     }
 }
 
-}
-
 cudaError_t rsa_b200_fill_one(uint32_t* out, unsigned long long count, int s_io, int sms, cudaStream_t stream) {
     if (count == 0) return cudaSuccess;
     rsa_b200::fill_one_kernel<<<sms * 4, 256, 0, stream>>>(out, count, s_io);
