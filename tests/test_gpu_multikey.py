@@ -141,3 +141,11 @@ def test_keygen_end_to_end(R, nbits):
     c = R.rsa_modexp_batch(t, 65537, k["n"], nbits)
     y = R.rsa_modexp_batch(c, k["d"], k["n"], nbits)
     assert np.array_equal(host(y), m)
+
+
+@pytest.mark.parametrize("nbits", [64, 96, 1000])
+def test_keygen_odd_sizes(R, nbits):
+    k = R.rsa_keygen(nbits, 65537, seed=3)
+    assert k["n"].bit_length() == nbits and k["n"] == k["p"] * k["q"] and k["p"] != k["q"]
+    assert oracle.is_prime(k["p"]) and oracle.is_prime(k["q"])
+    assert oracle.keygen_check(k["p"], k["q"], 65537) == (k["n"], k["phi"], k["d"])

@@ -300,3 +300,19 @@ def test_paper_fig12_errors(R):
         with pytest.raises(R.RsaError) as ei:
             R.rsa_modexp_batch_paper(t, key, den)
         assert ei.value.code == R.RSA_ERANGE
+
+
+# ------------------------------------------------------------------ host entry on other classes
+
+@pytest.mark.parametrize("key,count", [("rsa4096", 2000), ("rsa64", 300001), ("toy17947", 5)])
+def test_host_entry_classes(R, key, count):
+    k = workload.key(key)
+    nb = k["n"].bit_length()
+    s = workload.limbs_needed(nb)
+    base = workload.packets(count, nb, n=k["n"], config_id=31) if nb > 20 else \
+        np.arange(count, dtype=np.uint32).reshape(-1, 1) + 7
+    out = R.rsa_modexp_batch_host(base, k["e"], k["n"], nb)
+    idx = np.unique(np.concatenate([np.arange(min(count, 8)), np.random.default_rng(1).choice(count, min(count, 300), replace=False)]))
+    assert np.array_equal(out[idx], oracle_rows(base[idx], k["e"], k["n"], s))
+    one = R.rsa_modexp_batch_host(base, 0, k["n"], nb)                 # exp = 0 -> 1
+    assert (one[:, 0] == 1).all() and (one[:, 1:] == 0).all()
