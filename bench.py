@@ -159,24 +159,6 @@ def ncu_traffic(key_name: str, leg: str, count: int):
     return None if not rec else rec["bytes_per_packet"] * count
 
 
-def _lib_text_enc(R, letters, e, n, nb, out, stream):
-    import ctypes
-    s = R.nlimbs(nb)
-    rc = R._lib.rsa_encrypt_text(ctypes.c_void_p(letters.data_ptr()), letters.numel(), R._p(R.limbs(e, s)),
-                                 R._p(R.limbs(n, s)), nb, ctypes.c_void_p(out.data_ptr()), None,
-                                 ctypes.c_void_p(stream.cuda_stream))
-    R._check(rc, "rsa_encrypt_text")
-
-
-def _lib_text_dec(R, cipher, d, n, nb, out, stream):
-    import ctypes
-    s = R.nlimbs(nb)
-    rc = R._lib.rsa_decrypt_text(ctypes.c_void_p(cipher.data_ptr()), cipher.shape[0], R._p(R.limbs(d, s)),
-                                 R._p(R.limbs(n, s)), nb, ctypes.c_void_p(out.data_ptr()), None,
-                                 ctypes.c_void_p(stream.cuda_stream))
-    R._check(rc, "rsa_decrypt_text")
-
-
 # ------------------------------------------------------------------ arms
 
 def run_reference(args, rank, world):
@@ -285,9 +267,9 @@ def run_ours(args, rank, world, local_rank):
                 R.rsa_modexp_batch_multi(bufs[j], expt, mods, nb, exp_bits=e.bit_length(), out=bufs[j + 1],
                                          stream=stream)
             elif kind == "text" and j == 0:
-                _lib_text_enc(R, bufs[0], e, n, nb, bufs[1], stream)
+                R.rsa_encrypt_text(bufs[0], e, n, nb, out=bufs[1], stream=stream)
             elif kind == "text":
-                _lib_text_dec(R, bufs[1], e, n, nb, bufs[2], stream)
+                R.rsa_decrypt_text(bufs[1], e, n, nb, out=bufs[2], stream=stream)
             elif kind == "crt":
                 R.rsa_decrypt_crt_batch(bufs[j], key["p"], key["q"], key["d"], nb, out=bufs[j + 1], stream=stream)
             else:

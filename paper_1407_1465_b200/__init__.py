@@ -157,14 +157,15 @@ def rsa_decrypt_crt_batch(c, p: int, q: int, d: int, nbits: int, out=None, strea
     return out
 
 
-def rsa_encrypt_text(text, e: int, n: int, nbits: int, status=None, stream=None):
+def rsa_encrypt_text(text, e: int, n: int, nbits: int, status=None, out=None, stream=None):
     """Fused sec. 2 codec + encryption.  text: CUDA uint8 tensor of lowercase
     letters (spaces stripped, even length) or a str; returns [count, s]."""
     import torch
     if isinstance(text, str):
         text = torch.tensor(list(text.replace(" ", "").encode("ascii")), dtype=torch.uint8, device="cuda")
     s = nlimbs(nbits)
-    out = torch.empty((text.numel() // 2, s), dtype=torch.int32, device=text.device)
+    if out is None:
+        out = torch.empty((text.numel() // 2, s), dtype=torch.int32, device=text.device)
     with torch.cuda.device(text.device):
         rc = _lib.rsa_encrypt_text(_vp(text.data_ptr()), text.numel(), _p(limbs(e, s)), _p(limbs(n, s)), nbits,
                                    _vp(out.data_ptr()), _vp(status.data_ptr() if status is not None else 0),
@@ -173,12 +174,13 @@ def rsa_encrypt_text(text, e: int, n: int, nbits: int, status=None, stream=None)
     return out
 
 
-def rsa_decrypt_text(cipher, d: int, n: int, nbits: int, status=None, stream=None):
+def rsa_decrypt_text(cipher, d: int, n: int, nbits: int, status=None, out=None, stream=None):
     """Fused decryption + sec. 2 decoding; returns a CUDA uint8 tensor of letters."""
     import torch
     s = nlimbs(nbits)
     cipher = cipher.contiguous()
-    out = torch.empty(2 * cipher.shape[0], dtype=torch.uint8, device=cipher.device)
+    if out is None:
+        out = torch.empty(2 * cipher.shape[0], dtype=torch.uint8, device=cipher.device)
     with torch.cuda.device(cipher.device):
         rc = _lib.rsa_decrypt_text(_vp(cipher.data_ptr()), cipher.shape[0], _p(limbs(d, s)), _p(limbs(n, s)), nbits,
                                    _vp(out.data_ptr()), _vp(status.data_ptr() if status is not None else 0),
