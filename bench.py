@@ -116,6 +116,19 @@ class ClockSampler:
                     if v.lower().startswith("active"):
                         reasons.add(nm)
         os.unlink(self.path)
+        if not sm:
+            # timed region shorter than nvidia-smi's start-up: one direct query
+            try:
+                q = subprocess.run(["nvidia-smi", "-i", str(self.index), "--query-gpu=" + ",".join(self.FIELDS),
+                                    "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=20)
+                parts = [p.strip() for p in q.stdout.strip().split(",")]
+                sm, smax, power = [float(parts[0])], [float(parts[1])], [float(parts[6])]
+                for nm, v in zip(names, parts[2:6]):
+                    if v.lower().startswith("active"):
+                        reasons.add(nm)
+                reasons.add("sampled-after-timed-region")
+            except (OSError, ValueError, IndexError, subprocess.TimeoutExpired):
+                pass
         loaded = [c for c in sm if smax and c > 0.5 * max(smax)] or sm
         return {"sm_mhz": statistics.median(loaded) if loaded else None,
                 "sm_max_mhz": max(smax) if smax else None,
