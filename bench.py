@@ -116,6 +116,7 @@ class ClockSampler:
                     if v.lower().startswith("active"):
                         reasons.add(nm)
         os.unlink(self.path)
+        note = None
         if not sm:
             # timed region shorter than nvidia-smi's start-up: one direct query
             try:
@@ -126,14 +127,17 @@ class ClockSampler:
                 for nm, v in zip(names, parts[2:6]):
                     if v.lower().startswith("active"):
                         reasons.add(nm)
-                reasons.add("sampled-after-timed-region")
+                note = "single sample after the timed region (shorter than nvidia-smi start-up)"
             except (OSError, ValueError, IndexError, subprocess.TimeoutExpired):
                 pass
         loaded = [c for c in sm if smax and c > 0.5 * max(smax)] or sm
-        return {"sm_mhz": statistics.median(loaded) if loaded else None,
-                "sm_max_mhz": max(smax) if smax else None,
-                "reasons": sorted(reasons), "samples": len(sm),
-                "power_w_max": max(power) if power else None}
+        out = {"sm_mhz": statistics.median(loaded) if loaded else None,
+               "sm_max_mhz": max(smax) if smax else None,
+               "reasons": sorted(reasons), "samples": len(sm),
+               "power_w_max": max(power) if power else None}
+        if note:
+            out["note"] = note
+        return out
 
 
 # ------------------------------------------------------------------ oracle baseline
