@@ -183,15 +183,15 @@ modexp_pair_kernel(const __grid_constant__ ModexpParams<S> p) {
     uint4* const slots = neven_all + 2 * NQ;
     const int ppb = blockDim.x / 2;
     for (int i = threadIdx.x; i < 2 * NQ; i += blockDim.x) {
-        const int h = i / NQ, q = i % NQ, o = h * L + 8 * q;
+        const int q = i >> 1, h = i & 1, o = h * L + 8 * q;    // halves interleaved: [q][half]
         nodd_all[i] = make_uint4(p.n[o + 1], p.n[o + 3], p.n[o + 5], p.n[o + 7]);
         neven_all[i] = make_uint4(p.n[o], p.n[o + 2], p.n[o + 4], p.n[o + 6]);
     }
     __syncthreads();
     const int half = threadIdx.x & 1;
     const int pk = threadIdx.x >> 1;
-    const uint4* nodd4 = nodd_all + half * NQ;
-    const uint4* neven4 = neven_all + half * NQ;
+    const uint4* nodd4 = nodd_all + half;
+    const uint4* neven4 = neven_all + half;
     uint4* const bslot = slots + pk;
     const unsigned gpk = (blockIdx.x * blockDim.x + threadIdx.x) >> 1;
     const unsigned npk = (gridDim.x * blockDim.x) >> 1;

@@ -36,8 +36,10 @@ __device__ __forceinline__ uint4 lds128(const uint4* p) {
     return v;
 }
 
-// Lane-local n half in shared memory: nodd4[q] = n_l[8q+1, 8q+3, 8q+5, 8q+7],
-// neven4[q] = n_l[8q, 8q+2, 8q+4, 8q+6].
+// Lane-local n half in shared memory: nodd4[2q] = n_l[8q+1, 8q+3, 8q+5, 8q+7],
+// neven4[2q] = n_l[8q, 8q+2, 8q+4, 8q+6]; the two lanes' groups are
+// interleaved (16 B apart, different banks) so each LDS.128 of a warp -- two
+// distinct addresses -- is a single wavefront.
 template <int L>
 __device__ __forceinline__ void cios_step_pair(uint32_t (&X)[L], uint32_t (&Y)[L], uint32_t& hi,
                                                const uint32_t (&a)[L], uint32_t b,
@@ -67,7 +69,7 @@ __device__ __forceinline__ void cios_step_pair(uint32_t (&X)[L], uint32_t (&Y)[L
     // odd products m * n_j (j = 8q + 1, 3, 5, 7)
 #pragma unroll
     for (int q = 0; q < L / 8; q++) {
-        const uint4 v = lds128(nodd4 + q);
+        const uint4 v = lds128(nodd4 + 2 * q);
         const int j = 8 * q + 1;
         if (q == 0) mad_lo_cc(Y[0], v.x, m, Y[0]);
         else madc_lo_cc(Y[j - 1], v.x, m, Y[j - 1]);
@@ -83,7 +85,7 @@ __device__ __forceinline__ void cios_step_pair(uint32_t (&X)[L], uint32_t (&Y)[L
     // even products m * n_j (j = 8q, 8q + 2, 4, 6); lane 0's X[0] becomes 0
 #pragma unroll
     for (int q = 0; q < L / 8; q++) {
-        const uint4 v = lds128(neven4 + q);
+        const uint4 v = lds128(neven4 + 2 * q);
         const int j = 8 * q;
         if (q == 0) mad_lo_cc(X[0], v.x, m, X[0]);
         else madc_lo_cc(X[j], v.x, m, X[j]);
@@ -145,9 +147,12 @@ __device__ __forceinline__ void montmul_pair(uint32_t (&a)[L], const uint4* __re
     // phase 1 gives lane 0's borrow, phase 2 redoes lane 1 with it.
     const uint32_t* nodd = reinterpret_cast<const uint32_t*>(nodd4);
     const uint32_t* neven = reinterpret_cast<const uint32_t*>(neven4);
+    // limb k of this lane's n: odd/even array, group (k>>1)>>2 (stride 2 groups), component (k>>1)&3
+#define NLIMB(k) (((k) & 1) ? nodd[(((k) >> 1) >> 2) * 8 + (((k) >> 1) & 3)] \
+                            : neven[(((k) >> 1) >> 2) * 8 + (((k) >> 1) & 3)])
     sub_cc(a[0], X[0], neven[0]);
 #pragma unroll
-    for (int k = 1; k < L; k++) subc_cc(a[k], X[k], (k & 1) ? nodd[k >> 1] : neven[k >> 1]);
+    for (int k = 1; k < L; k++) subc_cc(a[k], X[k], NLIMB(k));
     uint32_t br;
     subc(br, 0u, 0u);                          // 0xFFFFFFFF if borrow
     const uint32_t b0 = __shfl_xor_sync(0xffffffffu, br, 1);
@@ -155,7 +160,8 @@ __device__ __forceinline__ void montmul_pair(uint32_t (&a)[L], const uint4* __re
     uint32_t dummy;
     sub_cc(dummy, 0u, bin);                     // sets the borrow flag iff bin
 #pragma unroll
-    for (int k = 0; k < L; k++) subc_cc(a[k], X[k], (k & 1) ? nodd[k >> 1] : neven[k >> 1]);
+    for (int k = 0; k < L; k++) subc_cc(a[k], X[k], NLIMB(k));
+#undef NLIMB
     uint32_t keep1;
     subc(keep1, hi, 0u);                        // lane 1: 0 if T >= n, 0xFFFFFFFF if T < n
     const uint32_t keep = __shfl_sync(0xffffffffu, keep1, src | 1);
