@@ -57,11 +57,12 @@ modexp_multi_kernel(const __grid_constant__ MultiParams p) {
     constexpr int NG = S / 4;
     constexpr int NQ = S / 8;
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    const int stride = blockDim.x;
+    constexpr int stride = MCfg<S>::BLOCK;       // launched with exactly this block size
+    using NS = NSharedT<stride>;
     uint4* const bslot = reinterpret_cast<uint4*>(smem_raw) + threadIdx.x;
     uint4* const nodd = reinterpret_cast<uint4*>(smem_raw) + NG * stride + threadIdx.x;
     uint4* const neven = nodd + NQ * stride;
-    const NShared nsh{nodd, neven, stride};
+    const NS nsh{nodd, neven};
     const unsigned gtid = blockIdx.x * blockDim.x + threadIdx.x;
     const unsigned nthr = gridDim.x * blockDim.x;
     const int w = p.window;
@@ -136,7 +137,7 @@ modexp_multi_kernel(const __grid_constant__ MultiParams p) {
 #pragma unroll
             for (int k = S - 1; k > 0; k--) sh[k] = (a[k] << 1) | (a[k - 1] >> 31);
             sh[0] = a[0] << 1;
-            const NShared& nn = nsh;
+            const NS& nn = nsh;
             uint32_t dd[S];
             sub_cc(dd[0], sh[0], nn.limb(0));
 #pragma unroll
@@ -246,8 +247,8 @@ modexp_multi_kernel(const __grid_constant__ MultiParams p) {
                 for (int k = 0; k < S; k++) { eq1 = eq1 && a[k] == one[k]; eqm = eqm && a[k] == mone[k]; }
                 prime = eq1 || eqm;
             }
-            if (sqr) montsqr_sm<S>(a, nsh, n0inv);
-            else montmul_sm<S>(a, bslot, stride, nsh, n0inv);
+            if (sqr) montsqr_sm<S, NS>(a, nsh, n0inv);
+            else montmul_sm<S, NS>(a, bslot, stride, nsh, n0inv);
             if (st >= K && st < s_scan) store_a(st - K + 1, a);   // T[1] .. T[nent-1]
             if (p.mode == 1 && st >= s_fin && st < my_total) {
                 bool e = true;

@@ -19,16 +19,19 @@ namespace rsa_b200 {
 // Per-thread n in shared memory: group q of the odd limbs
 // (n[8q+1], n[8q+3], n[8q+5], n[8q+7]) is at nodd[q * stride]; even limbs
 // (n[8q], n[8q+2], n[8q+4], n[8q+6]) at neven[q * stride].  S % 8 == 0.
-struct NShared {
+// STRIDE (uint4 elements between a thread's groups) is the block size, a
+// compile-time constant, so every address folds into an LDS immediate.
+template <int STRIDE>
+struct NSharedT {
     const uint4* nodd;
     const uint4* neven;
-    int stride;
-    __device__ __forceinline__ uint4 odd(int q) const { return ldsv(nodd + q * stride); }
-    __device__ __forceinline__ uint4 even(int q) const { return ldsv(neven + q * stride); }
+    static constexpr int stride = STRIDE;
+    __device__ __forceinline__ uint4 odd(int q) const { return ldsv(nodd + q * STRIDE); }
+    __device__ __forceinline__ uint4 even(int q) const { return ldsv(neven + q * STRIDE); }
     __device__ __forceinline__ uint32_t limb(int j) const {
         const uint32_t* p = reinterpret_cast<const uint32_t*>((j & 1) ? nodd : neven);
         const int k = j >> 1;                  // index among odd (even) limbs
-        return p[(k >> 2) * stride * 4 + (k & 3)];
+        return p[(k >> 2) * STRIDE * 4 + (k & 3)];
     }
     static __device__ __forceinline__ uint4 ldsv(const uint4* p) {
         uint4 v;
@@ -41,7 +44,7 @@ struct NShared {
 
 // T += m * n (odd limbs into Y, shifted as in the CIOS step when `rshift`;
 // in place otherwise) -- helpers for the chains below.
-template <int S>
+template <int S, class NShared>
 __device__ __forceinline__ void red_odd_inplace(uint32_t (&Y)[S], uint32_t& hi, uint32_t m, const NShared& n) {
 #pragma unroll
     for (int q = 0; q < S / 8; q++) {
@@ -60,7 +63,7 @@ __device__ __forceinline__ void red_odd_inplace(uint32_t (&Y)[S], uint32_t& hi, 
     addc(hi, hi, 0u);
 }
 
-template <int S>
+template <int S, class NShared>
 __device__ __forceinline__ void red_even_inplace(uint32_t (&X)[S], uint32_t (&Y)[S], uint32_t& hi, uint32_t m,
                                                  const NShared& n) {
 #pragma unroll
@@ -82,7 +85,7 @@ __device__ __forceinline__ void red_even_inplace(uint32_t (&X)[S], uint32_t (&Y)
 }
 
 // CIOS step with a per-thread n (cf. cios_step in mont.cuh)
-template <int S>
+template <int S, class NShared>
 __device__ __forceinline__ void cios_step_sm(uint32_t (&X)[S], uint32_t (&Y)[S], uint32_t& hi,
                                              const uint32_t (&a)[S], uint32_t b, const NShared& n, uint32_t n0inv) {
     add_cc(X[0], X[0], Y[1]);
@@ -104,12 +107,12 @@ __device__ __forceinline__ void cios_step_sm(uint32_t (&X)[S], uint32_t (&Y)[S],
     addc_cc(Y[S - 1], Y[S - 1], 0u);
     addc(hi, hi, 0u);
     const uint32_t m = X[0] * n0inv;
-    red_odd_inplace<S>(Y, hi, m, n);
-    red_even_inplace<S>(X, Y, hi, m, n);
+    red_odd_inplace<S, NShared>(Y, hi, m, n);
+    red_even_inplace<S, NShared>(X, Y, hi, m, n);
 }
 
 // reduction-only step with the shift done by the odd chain (cf. red_step)
-template <int S>
+template <int S, class NShared>
 __device__ __forceinline__ void red_step_sm(uint32_t (&X)[S], uint32_t (&Y)[S], uint32_t& hi, const NShared& n,
                                             uint32_t n0inv) {
     add_cc(X[0], X[0], Y[1]);
@@ -133,11 +136,11 @@ __device__ __forceinline__ void red_step_sm(uint32_t (&X)[S], uint32_t (&Y)[S], 
         }
     }
     addc(hi, 0u, 0u);
-    red_even_inplace<S>(X, Y, hi, m, n);
+    red_even_inplace<S, NShared>(X, Y, hi, m, n);
 }
 
 // merge (X, Y pre-shift, hi) + optional addend, conditional subtract -> a
-template <int S>
+template <int S, class NShared>
 __device__ __forceinline__ void finish_sm(uint32_t (&a)[S], uint32_t (&X)[S], uint32_t (&Y)[S], uint32_t hi,
                                           const uint32_t* addend, const NShared& n) {
     add_cc(X[0], X[0], Y[1]);
@@ -168,9 +171,10 @@ __device__ __forceinline__ void finish_sm(uint32_t (&a)[S], uint32_t (&X)[S], ui
 }
 
 // A <- A * B R^-1 mod n (B in this thread's smem slot, group g at bslot[g*stride])
-template <int S>
-__device__ __forceinline__ void montmul_sm(uint32_t (&a)[S], const uint4* __restrict__ bslot, int stride,
+template <int S, class NShared>
+__device__ __forceinline__ void montmul_sm(uint32_t (&a)[S], const uint4* __restrict__ bslot, int /*stride*/,
                                            const NShared& n, uint32_t n0inv) {
+    constexpr int stride = NShared::stride;
     uint32_t X[S], Y[S], hi = 0;
 #pragma unroll
     for (int k = 0; k < S; k++) { X[k] = 0; Y[k] = 0; }
@@ -179,17 +183,17 @@ __device__ __forceinline__ void montmul_sm(uint32_t (&a)[S], const uint4* __rest
 #pragma unroll
         for (int g = g0; g < g0 + 2; g++) {
             const uint4 bv = bslot[g * stride];
-            cios_step_sm<S>(X, Y, hi, a, bv.x, n, n0inv);
-            cios_step_sm<S>(Y, X, hi, a, bv.y, n, n0inv);
-            cios_step_sm<S>(X, Y, hi, a, bv.z, n, n0inv);
-            cios_step_sm<S>(Y, X, hi, a, bv.w, n, n0inv);
+            cios_step_sm<S, NShared>(X, Y, hi, a, bv.x, n, n0inv);
+            cios_step_sm<S, NShared>(Y, X, hi, a, bv.y, n, n0inv);
+            cios_step_sm<S, NShared>(X, Y, hi, a, bv.z, n, n0inv);
+            cios_step_sm<S, NShared>(Y, X, hi, a, bv.w, n, n0inv);
         }
     }
-    finish_sm<S>(a, X, Y, hi, nullptr, n);
+    finish_sm<S, NShared>(a, X, Y, hi, nullptr, n);
 }
 
 // A <- A^2 R^-1 mod n (triangle of mont_sqr.cuh, reduction with smem n)
-template <int S>
+template <int S, class NShared>
 __device__ __forceinline__ void montsqr_sm(uint32_t (&a)[S], const NShared& n, uint32_t n0inv) {
     uint32_t T[2 * S];
     square_full<S>(a, T);
@@ -198,16 +202,16 @@ __device__ __forceinline__ void montsqr_sm(uint32_t (&a)[S], const NShared& n, u
     for (int k = 0; k < S; k++) { X[k] = T[k]; Y[k] = 0; }
 #pragma unroll 1
     for (int i = 0; i < S; i += 8) {
-        red_step_sm<S>(X, Y, hi, n, n0inv);
-        red_step_sm<S>(Y, X, hi, n, n0inv);
-        red_step_sm<S>(X, Y, hi, n, n0inv);
-        red_step_sm<S>(Y, X, hi, n, n0inv);
-        red_step_sm<S>(X, Y, hi, n, n0inv);
-        red_step_sm<S>(Y, X, hi, n, n0inv);
-        red_step_sm<S>(X, Y, hi, n, n0inv);
-        red_step_sm<S>(Y, X, hi, n, n0inv);
+        red_step_sm<S, NShared>(X, Y, hi, n, n0inv);
+        red_step_sm<S, NShared>(Y, X, hi, n, n0inv);
+        red_step_sm<S, NShared>(X, Y, hi, n, n0inv);
+        red_step_sm<S, NShared>(Y, X, hi, n, n0inv);
+        red_step_sm<S, NShared>(X, Y, hi, n, n0inv);
+        red_step_sm<S, NShared>(Y, X, hi, n, n0inv);
+        red_step_sm<S, NShared>(X, Y, hi, n, n0inv);
+        red_step_sm<S, NShared>(Y, X, hi, n, n0inv);
     }
-    finish_sm<S>(a, X, Y, hi, T + S, n);
+    finish_sm<S, NShared>(a, X, Y, hi, T + S, n);
 }
 
 }  // namespace rsa_b200
