@@ -166,6 +166,123 @@ modexp_kernel(const __grid_constant__ ModexpParams<S> p) {
 
 
 // ---------------------------------------------------------------------------
+// Small widths (S <= 4, 64- and 128-bit moduli, the toy keys): a montmul is
+// only 2S^2 + S = 10 (S = 2) products, comparable to the per-op decode and the
+// shared-memory staging of b.  Here each thread carries PPT packets: one op
+// decode serves PPT montmuls, b stays in registers, and the PPT independent
+// CIOS chains interleave (ILP).  Packet k of virtual slot (t, k) is
+// t * nthr * PPT + k * nthr + gtid, so every load/store and table access is
+// coalesced per k; the window table is indexed by virtual slot k * nthr + gtid.
+template <int S> struct SmallCfg { static constexpr int PPT = (S <= 2) ? 4 : 2; };
+
+template <int S, int IO = 0>
+__global__ void __launch_bounds__(128)
+modexp_small_kernel(const __grid_constant__ ModexpParams<S> p) {
+    using V = typename BVec<S>::T;               // one table entry (S <= 4: one vector)
+    constexpr int PPT = SmallCfg<S>::PPT;
+    static_assert(S <= 4, "small-width kernel");
+    const unsigned gtid = blockIdx.x * blockDim.x + threadIdx.x;
+    const unsigned nthr = gridDim.x * blockDim.x;
+    const unsigned long long nvs = (unsigned long long)nthr * PPT;     // virtual slots
+    V* const table = reinterpret_cast<V*>(p.table);
+    const unsigned long long trips = (p.count + nvs - 1) / nvs;
+    for (unsigned long long t = 0; t < trips; t++) {
+        uint32_t a[PPT][S];
+        unsigned long long pkt[PPT];
+        bool valid[PPT];
+        int io_status[PPT];
+#pragma unroll
+        for (int k = 0; k < PPT; k++) {
+            const unsigned long long p0 = t * nvs + (unsigned long long)k * nthr + gtid;
+            valid[k] = p0 < p.count;
+            pkt[k] = valid[k] ? p0 : p.count - 1;
+            io_status[k] = 0;
+            if constexpr (IO == 1) {
+                const uchar2 ch = reinterpret_cast<const uchar2*>(p.base)[pkt[k]];
+                const uint32_t hi = (uint32_t)ch.x - 'a', lo = (uint32_t)ch.y - 'a';
+                if (hi > 25u || lo > 25u) io_status[k] = -7;
+#pragma unroll
+                for (int j = 0; j < S; j++) a[k][j] = 0u;
+                a[k][0] = (io_status[k] ? 0u : hi * 100u + lo);
+            } else {
+                const uint32_t* src = p.base + pkt[k] * (unsigned long long)p.s_io;
+#pragma unroll
+                for (int j = 0; j < S; j++) a[k][j] = (j < p.s_io) ? __ldg(src + j) : 0u;
+            }
+        }
+        for (int i = 0; i < p.nops; i++) {
+            const RsaOp op = p.ops[i];
+            if (op.flags & RSA_F_LOADA) {
+#pragma unroll
+                for (int k = 0; k < PPT; k++) {
+                    const V v = table[(size_t)op.lidx * nvs + (size_t)k * nthr + gtid];
+                    a[k][0] = v.x; a[k][1] = v.y;
+                    if constexpr (S == 4) { a[k][2] = v.z; a[k][3] = v.w; }
+                }
+            }
+            if (op.kind == RSA_OP_SQR) {
+                for (int r = 0; r < op.rep; r++) {
+#pragma unroll
+                    for (int k = 0; k < PPT; k++) montmul_regb<S>(a[k], a[k], p.n, p.n0inv);
+                }
+            } else {
+                uint32_t b[PPT][S];
+#pragma unroll
+                for (int k = 0; k < PPT; k++) {
+                    if (op.kind == RSA_OP_MUL) {
+                        const V v = table[(size_t)op.bidx * nvs + (size_t)k * nthr + gtid];
+                        b[k][0] = v.x; b[k][1] = v.y;
+                        if constexpr (S == 4) { b[k][2] = v.z; b[k][3] = v.w; }
+                    } else {
+#pragma unroll
+                        for (int j = 0; j < S; j++)
+                            b[k][j] = (op.kind == RSA_OP_R2) ? p.r2[j] : (j == 0 ? 1u : 0u);
+                    }
+                }
+                for (int r = 0; r < op.rep; r++) {
+#pragma unroll
+                    for (int k = 0; k < PPT; k++) montmul_regb<S>(a[k], b[k], p.n, p.n0inv);
+                }
+            }
+            if (op.flags & RSA_F_STORE) {
+#pragma unroll
+                for (int k = 0; k < PPT; k++) {
+                    V v; v.x = a[k][0]; v.y = a[k][1];
+                    if constexpr (S == 4) { v.z = a[k][2]; v.w = a[k][3]; }
+                    table[(size_t)op.sidx * nvs + (size_t)k * nthr + gtid] = v;
+                }
+            }
+        }
+#pragma unroll
+        for (int k = 0; k < PPT; k++) {
+            if (!valid[k]) continue;
+            if constexpr (IO == 2) {
+                bool high = false;
+#pragma unroll
+                for (int j = 1; j < S; j++) high = high || a[k][j] != 0u;
+                const uint32_t hi = a[k][0] / 100u, lo = a[k][0] % 100u;
+                uchar2 ch;
+                if (high || hi > 25u || lo > 25u) {
+                    io_status[k] = -10;
+                    ch = make_uchar2('?', '?');
+                } else {
+                    ch = make_uchar2((unsigned char)('a' + hi), (unsigned char)('a' + lo));
+                }
+                reinterpret_cast<uchar2*>(p.out)[pkt[k]] = ch;
+            } else {
+                uint32_t* dst = p.out + pkt[k] * (unsigned long long)p.s_io;
+#pragma unroll
+                for (int j = 0; j < S; j++)
+                    if (j < p.s_io) dst[j] = a[k][j];
+            }
+            if constexpr (IO != 0) {
+                if (p.status) p.status[pkt[k]] = io_status[k];
+            }
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
 // S = 2L limbs (4096-bit class): two lanes per packet (mont_pair.cuh).  Every
 // thread runs the same number of trips so each warp stays converged (the
 // pair shuffles use the full mask); out-of-range trips recompute the last
@@ -493,6 +610,29 @@ static cudaError_t launch_class(const void* params, int sms, cudaStream_t stream
     return cudaGetLastError();
 }
 
+template <int S, int IO = 0>
+static cudaError_t launch_small(const void* params, int sms, cudaStream_t stream, int* grid_out, int* block_out,
+                                size_t* tab_stride_out, bool query_only) {
+    constexpr int PPT = SmallCfg<S>::PPT;
+    const int block = 128;
+    static int occ = -1;
+    if (occ < 0) {
+        cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, modexp_small_kernel<S, IO>, block, 0);
+        if (e != cudaSuccess) return e;
+        if (occ < 1) occ = 1;
+    }
+    int grid = sms * occ;
+    if (grid_out) *grid_out = grid;
+    if (block_out) *block_out = block;
+    if (tab_stride_out) *tab_stride_out = (size_t)grid * block * PPT;
+    if (query_only) return cudaSuccess;
+    const ModexpParams<S>& prm = *static_cast<const ModexpParams<S>*>(params);
+    const unsigned long long need = (prm.count + (unsigned long long)block * PPT - 1) / ((unsigned long long)block * PPT);
+    if (need < (unsigned long long)grid) grid = (int)need;
+    modexp_small_kernel<S, IO><<<grid, block, 0, stream>>>(prm);
+    return cudaGetLastError();
+}
+
 }  // namespace rsa_b200
 
 // Lanes per packet for the 4096-bit class: 2 (default, mont_pair.cuh) or 4
@@ -509,6 +649,17 @@ static int rsa_b200_shape64() {
     return v;
 }
 
+// Small widths (S = 2, 4): multi-packet-per-thread kernel (default) or the
+// thread-per-packet kernel with smem-staged b (RSA_B200_SMALL=0), for A/B.
+static bool rsa_b200_small() {
+    static int v = -1;
+    if (v < 0) {
+        const char* e = getenv("RSA_B200_SMALL");
+        v = (e && e[0] == '0') ? 0 : 1;
+    }
+    return v == 1;
+}
+
 static int rsa_b200_tpi128() {
     static int v = 0;
     if (!v) {
@@ -519,11 +670,24 @@ static int rsa_b200_tpi128() {
 }
 
 // Host entry points used by rsa_abi.cpp (C++ linkage, not part of the C-ABI).
+
+// 1 if class S runs squarings through the dedicated montsqr (1.5 S^2 + 1.5 S
+// products), 0 if through CIOS (2 S^2 + S): the small-width, group and pair
+// kernels have no squaring path.  Used for the window choice and the
+// executed-product count of rsa_plan_info.
+int rsa_b200_sqr_dedicated(int S) {
+    if (S <= 4) return rsa_b200_small() ? 0 : 1;
+    if (S == 64) return rsa_b200_shape64() ? 0 : 1;
+    return S <= 64 ? 1 : 0;
+}
+
 cudaError_t rsa_b200_launch(int S, const void* params, int sms, cudaStream_t stream) {
     using namespace rsa_b200;
     switch (S) {
-    case 2: return launch_class<2>(params, sms, stream, nullptr, nullptr, nullptr, false);
-    case 4: return launch_class<4>(params, sms, stream, nullptr, nullptr, nullptr, false);
+    case 2: return rsa_b200_small() ? launch_small<2>(params, sms, stream, nullptr, nullptr, nullptr, false)
+                                    : launch_class<2>(params, sms, stream, nullptr, nullptr, nullptr, false);
+    case 4: return rsa_b200_small() ? launch_small<4>(params, sms, stream, nullptr, nullptr, nullptr, false)
+                                    : launch_class<4>(params, sms, stream, nullptr, nullptr, nullptr, false);
     case 8: return launch_class<8>(params, sms, stream, nullptr, nullptr, nullptr, false);
     case 16: return launch_class<16>(params, sms, stream, nullptr, nullptr, nullptr, false);
     case 32: return launch_class<32>(params, sms, stream, nullptr, nullptr, nullptr, false);
@@ -539,6 +703,10 @@ cudaError_t rsa_b200_launch(int S, const void* params, int sms, cudaStream_t str
 // codec-fused launches (S = 2 class only): io = 1 text in, io = 2 text out
 cudaError_t rsa_b200_launch_codec(const void* params, int io, int sms, cudaStream_t stream) {
     using namespace rsa_b200;
+    if (rsa_b200_small()) {
+        if (io == 1) return launch_small<2, 1>(params, sms, stream, nullptr, nullptr, nullptr, false);
+        if (io == 2) return launch_small<2, 2>(params, sms, stream, nullptr, nullptr, nullptr, false);
+    }
     if (io == 1) return launch_class<2, 1>(params, sms, stream, nullptr, nullptr, nullptr, false);
     if (io == 2) return launch_class<2, 2>(params, sms, stream, nullptr, nullptr, nullptr, false);
     return cudaErrorInvalidValue;
@@ -548,8 +716,10 @@ cudaError_t rsa_b200_launch_codec(const void* params, int io, int sms, cudaStrea
 cudaError_t rsa_b200_grid(int S, int sms, int* grid, int* block, size_t* nthreads) {
     using namespace rsa_b200;
     switch (S) {
-    case 2: return launch_class<2>(nullptr, sms, 0, grid, block, nthreads, true);
-    case 4: return launch_class<4>(nullptr, sms, 0, grid, block, nthreads, true);
+    case 2: return rsa_b200_small() ? launch_small<2>(nullptr, sms, 0, grid, block, nthreads, true)
+                                    : launch_class<2>(nullptr, sms, 0, grid, block, nthreads, true);
+    case 4: return rsa_b200_small() ? launch_small<4>(nullptr, sms, 0, grid, block, nthreads, true)
+                                    : launch_class<4>(nullptr, sms, 0, grid, block, nthreads, true);
     case 8: return launch_class<8>(nullptr, sms, 0, grid, block, nthreads, true);
     case 16: return launch_class<16>(nullptr, sms, 0, grid, block, nthreads, true);
     case 32: return launch_class<32>(nullptr, sms, 0, grid, block, nthreads, true);

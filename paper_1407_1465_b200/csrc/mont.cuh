@@ -113,6 +113,26 @@ __device__ __forceinline__ void cios_step(uint32_t (&X)[S], uint32_t (&Y)[S], ui
     addc(hi, hi, 0u);
 }
 
+// After S CIOS iterations (S even, so X is even-aligned again):
+// merge r = X + (Y pre-shift) + hi * 2^(32 S), then the conditional
+// subtraction r - n (keep r if it borrowed) -> a, canonical in [0, n).
+template <int S>
+__device__ __forceinline__ void mont_finish(uint32_t (&a)[S], uint32_t (&X)[S], const uint32_t (&Y)[S], uint32_t hi,
+                                            const uint32_t* __restrict__ n) {
+    add_cc(X[0], X[0], Y[1]);
+#pragma unroll
+    for (int k = 1; k + 1 < S; k++) addc_cc(X[k], X[k], Y[k + 1]);
+    addc_cc(X[S - 1], X[S - 1], 0u);
+    addc(hi, hi, 0u);
+    sub_cc(a[0], X[0], n[0]);
+#pragma unroll
+    for (int k = 1; k < S; k++) subc_cc(a[k], X[k], n[k]);
+    uint32_t keep;
+    subc(keep, hi, 0u);               // 0 if r >= n, 0xFFFFFFFF if r < n
+#pragma unroll
+    for (int k = 0; k < S; k++) a[k] = (X[k] & keep) | (a[k] & ~keep);
+}
+
 template <int S> struct BVec;
 template <> struct BVec<2> { typedef uint2 T; static constexpr int G = 2; };
 template <int S> struct BVec { typedef uint4 T; static constexpr int G = 4; };
@@ -155,20 +175,24 @@ __device__ __forceinline__ void montmul(uint32_t (&a)[S], const typename BVec<S>
         }
     }
 
-    // merge: r = X + (Y pre-shift) + hi * 2^(32 S)   (into X, top word in hi)
-    add_cc(X[0], X[0], Y[1]);
+    mont_finish<S>(a, X, Y, hi, n);
+}
+
+// A <- A * B * R^-1 mod n with B in registers (small widths: no shared-memory
+// staging; B may alias A -- every B word is read before A is written).
+template <int S>
+__device__ __forceinline__ void montmul_regb(uint32_t (&a)[S], const uint32_t (&b)[S],
+                                             const uint32_t* __restrict__ n, uint32_t n0inv) {
+    static_assert(S % 2 == 0, "S must be even");
+    uint32_t X[S], Y[S], hi = 0;
 #pragma unroll
-    for (int k = 1; k + 1 < S; k++) addc_cc(X[k], X[k], Y[k + 1]);
-    addc_cc(X[S - 1], X[S - 1], 0u);
-    addc(hi, hi, 0u);
-    // conditional subtraction: d = r - n; keep r if it borrowed
-    sub_cc(a[0], X[0], n[0]);
+    for (int k = 0; k < S; k++) { X[k] = 0; Y[k] = 0; }
 #pragma unroll
-    for (int k = 1; k < S; k++) subc_cc(a[k], X[k], n[k]);
-    uint32_t keep;
-    subc(keep, hi, 0u);               // 0 if r >= n, 0xFFFFFFFF if r < n
-#pragma unroll
-    for (int k = 0; k < S; k++) a[k] = (X[k] & keep) | (a[k] & ~keep);
+    for (int i = 0; i < S; i += 2) {
+        cios_step<S>(X, Y, hi, a, b[i], n, n0inv);
+        cios_step<S>(Y, X, hi, a, b[i + 1], n, n0inv);
+    }
+    mont_finish<S>(a, X, Y, hi, n);
 }
 
 }  // namespace rsa_b200

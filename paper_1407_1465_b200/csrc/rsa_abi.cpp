@@ -25,6 +25,7 @@
 cudaError_t rsa_b200_launch(int S, const void* params, int sms, cudaStream_t stream);
 cudaError_t rsa_b200_launch_codec(const void* params, int io, int sms, cudaStream_t stream);
 cudaError_t rsa_b200_grid(int S, int sms, int* grid, int* block, size_t* nthreads);
+int rsa_b200_sqr_dedicated(int S);
 cudaError_t rsa_b200_fill_one(uint32_t* out, unsigned long long count, int s_io, int sms, cudaStream_t stream);
 cudaError_t rsa_b200_multi(int S, const uint32_t* base, const uint32_t* exps, const uint32_t* mods, uint32_t* out,
                            int32_t* status, void* table, unsigned long long count, int s_io, int exp_bits,
@@ -232,9 +233,9 @@ static int get_plan_ptr(const uint32_t* exp, const uint32_t* n, int nbits, std::
             long long mm, sq;
             if (!build_ops(E, w, &ops, &ntab, &mm, &sq)) continue;
             // minimise executed limb products (squarings are cheaper when the
-            // dedicated squaring kernel is used, S <= 64)
+            // class has the dedicated squaring kernel)
             const long long S = pl.S;
-            const long long sqc = (pl.S <= 64) ? (3 * S * S + 3 * S) / 2 : 2 * S * S + S;
+            const long long sqc = rsa_b200_sqr_dedicated(pl.S) ? (3 * S * S + 3 * S) / 2 : 2 * S * S + S;
             const long long cost = sq * sqc + (mm - sq) * (2 * S * S + S);
             if (best < 0 || cost < best) {
                 best = cost;
@@ -593,7 +594,7 @@ int rsa_plan_info(const uint32_t* exp, const uint32_t* n, int nbits, rsa_plan_in
     info->squarings = pl.squarings;
     info->exp_bits = pl.exp_bits;
     const long long S = pl.S;
-    info->sqr_kernel = (pl.S <= 64) ? 1 : 0;     // modexp.cu: montsqr for S <= 64
+    info->sqr_kernel = rsa_b200_sqr_dedicated(pl.S);   // modexp.cu: which kernel runs class S
     const long long sq_cost = info->sqr_kernel ? (3 * S * S + 3 * S) / 2 : 2 * S * S + S;
     info->products = pl.squarings * sq_cost + (pl.montmuls - pl.squarings) * (2 * S * S + S);
     const int sms = device_sms();

@@ -1,6 +1,8 @@
 """The alternative kernel shapes kept for measurement ('chosen by
 measurement'): 2048-bit as a 2-lane group (RSA_B200_SHAPE64=group2) and
-4096-bit as a 4-lane group (RSA_B200_TPI128=4) stay bit-exact vs the oracle.
+4096-bit as a 4-lane group (RSA_B200_TPI128=4), and the thread-per-packet
+kernel for the small widths (RSA_B200_SMALL=0, instead of the multi-packet
+one) stay bit-exact vs the oracle.
 Run in subprocesses (the switch is read once per process)."""
 import os
 import subprocess
@@ -28,7 +30,10 @@ print("shape ok")
 @pytest.mark.parametrize("env,key,count", [("RSA_B200_SHAPE64=group2", "rsa2048", 300),
                                            ("RSA_B200_SHAPE64=group2", "rsa1536", 300),
                                            ("RSA_B200_TPI128=4", "rsa4096", 60),
-                                           ("RSA_B200_TPI128=4", "rsa3072", 60)])
+                                           ("RSA_B200_TPI128=4", "rsa3072", 60),
+                                           ("RSA_B200_SMALL=0", "rsa64", 3001),
+                                           ("RSA_B200_SMALL=0", "rsa128", 3001),
+                                           ("RSA_B200_SMALL=0", "toy17947", 3001)])
 def test_alternative_shapes(env, key, count):
     torch = pytest.importorskip("torch")
     if not torch.cuda.is_available():
