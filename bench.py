@@ -163,6 +163,18 @@ def cpu_baseline(key: dict, base: np.ndarray, legs, cpu_seconds: float):
                       f"({', '.join(l for l, _ in legs)}); {wall:.1f} s wall on {cores} threads"}
 
 
+def batch_kernel_name(S: int) -> str:
+    """The kernel modexp.cu launches for width class S (same env switches)."""
+    if S <= 4 and os.environ.get("RSA_B200_SMALL", "1")[:1] != "0":
+        return f"modexp_small_kernel<{S}>"
+    if S == 64 and os.environ.get("RSA_B200_SHAPE64", "")[:1] == "g":
+        return "modexp_group_kernel<64, 2>"
+    if S == 128:
+        return "modexp_group_kernel<128, 4>" if os.environ.get("RSA_B200_TPI128", "")[:1] == "4" \
+            else "modexp_pair_kernel<128>"
+    return f"modexp_kernel<{S}>"
+
+
 def ncu_traffic(key_name: str, leg: str, count: int):
     """DRAM bytes (read + write) per launch of the dominant kernel, from the
     committed ncu --set full capture (profiles/ncu_traffic.json, bytes per
@@ -375,7 +387,7 @@ def run_ours(args, rank, world, local_rank):
                 "traffic_unit": "bytes per launch", "algorithmic_bytes": count * s * 4 * 2,
                 "kernel": ({"multi": f"modexp_multi_kernel<{S}>", "mr": f"modexp_multi_kernel<{S}> (MR mode)",
                             "crt": f"2 x modexp_kernel<{S}> + crt_split/combine (half-width CRT legs; products of both)"}.get(
-                    kind, f"modexp_pair_kernel<{S}>" if S == 128 else f"modexp_kernel<{S}>")) + f" ({legs[dom][0]})",
+                    kind, batch_kernel_name(S))) + f" ({legs[dom][0]})",
                 "algorithmic": f"{plans[dom]['products']} 32x32->64 limb products/packet "
                                f"({plans[dom]['squarings']} squarings x "
                                f"{'1.5S^2+1.5S' if plans[dom]['sqr_kernel'] else '2S^2+S'} + "

@@ -25,7 +25,8 @@ def stale() -> bool:
 def build(force: bool = False, verbose: bool = False) -> str:
     if not force and not stale():
         return LIB
-    cmd = [NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-shared", "-Xcompiler", "-fPIC",
+    extra = os.environ.get("RSA_B200_NVCC_EXTRA", "").split()   # A/B experiments, e.g. -DRSA_SMALL_PPT2=8
+    cmd = [NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-shared", "-Xcompiler", "-fPIC", *extra,
            "-Xptxas", "-v" if verbose else "-O3", "-o", LIB + ".tmp", *SOURCES]
     subprocess.check_call(cmd)
     os.replace(LIB + ".tmp", LIB)

@@ -173,7 +173,13 @@ modexp_kernel(const __grid_constant__ ModexpParams<S> p) {
 // CIOS chains interleave (ILP).  Packet k of virtual slot (t, k) is
 // t * nthr * PPT + k * nthr + gtid, so every load/store and table access is
 // coalesced per k; the window table is indexed by virtual slot k * nthr + gtid.
-template <int S> struct SmallCfg { static constexpr int PPT = (S <= 2) ? 4 : 2; };
+#ifndef RSA_SMALL_PPT2
+#define RSA_SMALL_PPT2 4
+#endif
+#ifndef RSA_SMALL_PPT4
+#define RSA_SMALL_PPT4 2
+#endif
+template <int S> struct SmallCfg { static constexpr int PPT = (S <= 2) ? RSA_SMALL_PPT2 : RSA_SMALL_PPT4; };
 
 template <int S, int IO = 0>
 __global__ void __launch_bounds__(128)
