@@ -25,13 +25,25 @@
 
 namespace rsa_b200 {
 
+// resident-CTA bounds per class (__launch_bounds__ min blocks), overridable
+// at build time for A/B runs (build.py RSA_B200_NVCC_EXTRA)
+#ifndef RSA_MINB32
+#define RSA_MINB32 4
+#endif
+#ifndef RSA_MINB16
+#define RSA_MINB16 6
+#endif
+#ifndef RSA_MINB8
+#define RSA_MINB8 4
+#endif
+
 template <int S>
 struct KCfg {
     // S = 64: one 256-thread CTA per SM and a barrier per Montgomery op keep all
     // 8 warps of an SM on the same code lines (the squaring + multiply code is
     // larger than the instruction cache; drifting warps thrash it).
     static constexpr int BLOCK = (S >= 64) ? 256 : 128;
-    static constexpr int MINB = (S >= 64) ? 1 : (S >= 32 ? 3 : 4);
+    static constexpr int MINB = (S >= 64) ? 1 : (S >= 32 ? RSA_MINB32 : (S >= 16 ? RSA_MINB16 : RSA_MINB8));
     static constexpr bool LOCKSTEP = (S >= 32);
 };
 
