@@ -15,7 +15,9 @@ Calls (same names as the C-ABI):
 """
 from __future__ import annotations
 
+import contextlib
 import ctypes
+import functools
 import os
 
 import numpy as np
@@ -97,6 +99,24 @@ def limbs(x: int, n: int) -> np.ndarray:
     return np.frombuffer(int(x).to_bytes(4 * n, "little"), dtype="<u4").astype(np.uint32)
 
 
+@functools.lru_cache(maxsize=256)
+def _climbs(x: int, n: int) -> np.ndarray:
+    """limbs() for the per-call key arguments (exp, n, ...), cached read-only:
+    the same key is converted once, not on every batch."""
+    a = limbs(x, n)
+    a.flags.writeable = False
+    return a
+
+
+def _on(device):
+    """Make `device` current for the call unless it already is (entering
+    torch.cuda.device costs two device switches per call)."""
+    import torch
+    if device.index is None or device.index == torch.cuda.current_device():
+        return contextlib.nullcontext()
+    return torch.cuda.device(device)
+
+
 def to_int(a) -> int:
     return int.from_bytes(np.ascontiguousarray(a, dtype="<u4").tobytes(), "little")
 
@@ -132,8 +152,8 @@ def rsa_modexp_batch(base, exp: int, n: int, nbits: int, out=None, stream=None):
         stream = torch.cuda.current_stream(base.device).cuda_stream
     elif hasattr(stream, "cuda_stream"):
         stream = stream.cuda_stream
-    E, N = limbs(exp, s), limbs(n, s)
-    with torch.cuda.device(base.device):
+    E, N = _climbs(exp, s), _climbs(n, s)
+    with _on(base.device):
         rc = _lib.rsa_modexp_batch(ctypes.c_void_p(base.data_ptr()), _p(E), _p(N), nbits, base.shape[0],
                                    ctypes.c_void_p(out.data_ptr()), ctypes.c_void_p(stream))
     _check(rc, "rsa_modexp_batch")
@@ -150,7 +170,7 @@ def rsa_decrypt_crt_batch(c, p: int, q: int, d: int, nbits: int, out=None, strea
     if out is None:
         out = torch.empty_like(c)
     pl = nlimbs(max(p.bit_length(), q.bit_length(), 1))
-    with torch.cuda.device(c.device):
+    with _on(c.device):
         rc = _lib.rsa_decrypt_crt_batch(_vp(c.data_ptr()), _p(limbs(p, pl)), _p(limbs(q, pl)), pl, _p(limbs(d, s)),
                                         nbits, c.shape[0], _vp(out.data_ptr()), _vp(_stream_of(c, stream)))
     _check(rc, "rsa_decrypt_crt_batch")
@@ -166,7 +186,7 @@ def rsa_encrypt_text(text, e: int, n: int, nbits: int, status=None, out=None, st
     s = nlimbs(nbits)
     if out is None:
         out = torch.empty((text.numel() // 2, s), dtype=torch.int32, device=text.device)
-    with torch.cuda.device(text.device):
+    with _on(text.device):
         rc = _lib.rsa_encrypt_text(_vp(text.data_ptr()), text.numel(), _p(limbs(e, s)), _p(limbs(n, s)), nbits,
                                    _vp(out.data_ptr()), _vp(status.data_ptr() if status is not None else 0),
                                    _vp(_stream_of(text, stream)))
@@ -181,7 +201,7 @@ def rsa_decrypt_text(cipher, d: int, n: int, nbits: int, status=None, out=None, 
     cipher = cipher.contiguous()
     if out is None:
         out = torch.empty(2 * cipher.shape[0], dtype=torch.uint8, device=cipher.device)
-    with torch.cuda.device(cipher.device):
+    with _on(cipher.device):
         rc = _lib.rsa_decrypt_text(_vp(cipher.data_ptr()), cipher.shape[0], _p(limbs(d, s)), _p(limbs(n, s)), nbits,
                                    _vp(out.data_ptr()), _vp(status.data_ptr() if status is not None else 0),
                                    _vp(_stream_of(cipher, stream)))
@@ -214,7 +234,7 @@ def rsa_modexp_batch_paper(num, key: int, den: int, faithful: bool = True, out=N
         stream = torch.cuda.current_stream(num.device).cuda_stream
     elif hasattr(stream, "cuda_stream"):
         stream = stream.cuda_stream
-    with torch.cuda.device(num.device):
+    with _on(num.device):
         rc = _lib.rsa_modexp_batch_paper(ctypes.c_void_p(num.data_ptr()), key, den, num.numel(),
                                          ctypes.c_void_p(out.data_ptr()), 1 if faithful else 0, ctypes.c_void_p(stream))
     _check(rc, "rsa_modexp_batch_paper")
@@ -240,7 +260,7 @@ def rsa_modexp_batch_multi(base, exps, mods, nbits: int, exp_bits: int | None = 
     if out is None:
         out = torch.empty_like(base)
     exp_bits = 32 * s if exp_bits is None else exp_bits
-    with torch.cuda.device(base.device):
+    with _on(base.device):
         rc = _lib.rsa_modexp_batch_multi(_vp(base.data_ptr()), _vp(exps.data_ptr()), _vp(mods.data_ptr()), nbits,
                                          exp_bits, base.shape[0], _vp(out.data_ptr()),
                                          _vp(status.data_ptr() if status is not None else 0),
@@ -254,7 +274,7 @@ def rsa_miller_rabin_batch(cand, nbits: int, base: int, out=None, stream=None):
     cand = cand.contiguous()
     if out is None:
         out = torch.empty(cand.shape[0], dtype=torch.int32, device=cand.device)
-    with torch.cuda.device(cand.device):
+    with _on(cand.device):
         rc = _lib.rsa_miller_rabin_batch(_vp(cand.data_ptr()), nbits, cand.shape[0], base, _vp(out.data_ptr()),
                                          _vp(_stream_of(cand, stream)))
     _check(rc, "rsa_miller_rabin_batch")
@@ -264,7 +284,7 @@ def rsa_miller_rabin_batch(cand, nbits: int, base: int, out=None, stream=None):
 def rsa_prime_candidates(nbits: int, seed: int, first: int, count: int, device="cuda", stream=None):
     import torch
     out = torch.empty((count, nlimbs(nbits)), dtype=torch.int32, device=device)
-    with torch.cuda.device(out.device):
+    with _on(out.device):
         rc = _lib.rsa_prime_candidates(nbits, seed, first, count, _vp(out.data_ptr()), _vp(_stream_of(out, stream)))
     _check(rc, "rsa_prime_candidates")
     return out
@@ -274,7 +294,7 @@ def rsa_prime_sieve(cand, nbits: int, stream=None):
     import torch
     cand = cand.contiguous()
     out = torch.empty(cand.shape[0], dtype=torch.int32, device=cand.device)
-    with torch.cuda.device(cand.device):
+    with _on(cand.device):
         rc = _lib.rsa_prime_sieve(_vp(cand.data_ptr()), nbits, cand.shape[0], _vp(out.data_ptr()),
                                   _vp(_stream_of(cand, stream)))
     _check(rc, "rsa_prime_sieve")

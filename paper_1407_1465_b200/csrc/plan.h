@@ -13,6 +13,13 @@
 
 #define RSA_MAX_OPS 2048          // ops per plan (8 B each, kernel params)
 
+// Op capacity of class S.  A 32S-bit exponent needs at most 2 ops per bit at
+// w = 1 (a squaring run + a multiply), plus the table precompute (<= 65) and
+// the conversions, so small classes carry a small op array: the parameter
+// block (copied into every launch) shrinks from 16 KB to 1.2 KB at S = 2.
+// Plans that do not fit a window's op list skip that window (build_ops).
+constexpr int rsa_ops_cap(int S) { return (64 * S + 160 < RSA_MAX_OPS) ? 64 * S + 160 : RSA_MAX_OPS; }
+
 enum RsaOpKind : uint8_t {
     RSA_OP_SQR = 0,    // A <- A * A * R^-1
     RSA_OP_MUL = 1,    // A <- A * T[bidx] * R^-1   (T = per-thread window table)
@@ -50,7 +57,7 @@ struct ModexpParams {
     uint32_t n0inv;               // -n^-1 mod 2^32
     uint32_t n[S];                // modulus, zero padded to S limbs
     uint32_t r2[S];               // R^2 mod n, R = 2^(32 S)
-    RsaOp ops[RSA_MAX_OPS];
+    RsaOp ops[rsa_ops_cap(S)];
 };
 
 // host-visible summary of a plan (also exported through the C-ABI)

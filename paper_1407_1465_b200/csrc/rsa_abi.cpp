@@ -100,7 +100,8 @@ static int width_class(int s_io) {
 }
 
 // Build the op list for window width w; returns false if it does not fit.
-static bool build_ops(const BN& e, int w, std::vector<RsaOp>* ops, int* ntab, long long* mm, long long* sq) {
+static bool build_ops(const BN& e, int w, int cap, std::vector<RsaOp>* ops, int* ntab, long long* mm,
+                      long long* sq) {
     std::vector<Window> win = recode(e, w);
     const int nodd = 1 << (w - 1);
     const int g2 = nodd;                      // table index of g^2 (w > 1)
@@ -148,7 +149,7 @@ static bool build_ops(const BN& e, int w, std::vector<RsaOp>* ops, int* ntab, lo
     }
     // from Montgomery form (+ the initial load if the scan had one window)
     push(RSA_OP_ONE, 1, pending_load ? RSA_F_LOADA : 0, 0, first, 0);
-    return (int)ops->size() <= RSA_MAX_OPS;
+    return (int)ops->size() <= cap;
 }
 
 template <int S>
@@ -231,7 +232,7 @@ static int get_plan_ptr(const uint32_t* exp, const uint32_t* n, int nbits, std::
             std::vector<RsaOp> ops;
             int ntab;
             long long mm, sq;
-            if (!build_ops(E, w, &ops, &ntab, &mm, &sq)) continue;
+            if (!build_ops(E, w, rsa_ops_cap(pl.S), &ops, &ntab, &mm, &sq)) continue;
             // minimise executed limb products (squarings are cheaper when the
             // class has the dedicated squaring kernel)
             const long long S = pl.S;
