@@ -396,6 +396,16 @@ def run_ours(args, rank, world, local_rank):
                 "peak_basis": f"{R_PRODUCTS_PER_CLK_PER_SM} products/clk/SM (IMAD.WIDE half rate, "
                               f"profiles/r01_imad_peak.jsonl) x {sms} SMs x {f_max:.0f} MHz "
                               f"(MEASURED_PEAKS sm_max_mhz)"}
+    if kind == "batch":
+        # the window table is algorithmic state too: every entry written once,
+        # read by each window multiply (+ the A loads); per resident thread it is
+        # ntab x S limbs, larger than L2 at S = 64 / w = 7, so it streams to DRAM
+        pd = plans[dom]
+        touches = pd["table_entries"] + (pd["montmuls"] - pd["squarings"] - 2) + 2
+        roofline["algorithmic_table_bytes"] = count * S * 4 * touches
+        roofline["traffic_note"] = ("DRAM traffic = packet I/O + the per-thread sliding-window table "
+                                    f"({pd['table_entries']} entries x {S * 4} B, {touches} entry reads/writes per "
+                                    "packet); compare traffic with algorithmic_bytes + algorithmic_table_bytes")
     if clk and clk.get("sm_mhz"):
         roofline["frac_at_measured_clock"] = achieved / (R_PRODUCTS_PER_CLK_PER_SM * sms * clk["sm_mhz"] * 1e6 / 1e12)
     legs_out = {}
