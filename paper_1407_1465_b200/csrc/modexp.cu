@@ -193,6 +193,16 @@ modexp_kernel(const __grid_constant__ ModexpParams<S> p) {
 #endif
 template <int S> struct SmallCfg { static constexpr int PPT = (S <= 2) ? RSA_SMALL_PPT2 : RSA_SMALL_PPT4; };
 
+#ifndef RSA_SMALL_PS
+#define RSA_SMALL_PS 1
+#endif
+template <int S>
+__device__ __forceinline__ void small_montmul(uint32_t (&a)[S], const uint32_t (&b)[S], const uint32_t* __restrict__ n,
+                                              uint32_t n0inv) {
+    if constexpr (S == 2 && RSA_SMALL_PS) montmul2_ps(a, b, n, n0inv);
+    else montmul_regb<S>(a, b, n, n0inv);
+}
+
 template <int S, int IO = 0>
 __global__ void __launch_bounds__(128)
 modexp_small_kernel(const __grid_constant__ ModexpParams<S> p) {
@@ -241,7 +251,7 @@ modexp_small_kernel(const __grid_constant__ ModexpParams<S> p) {
             if (op.kind == RSA_OP_SQR) {
                 for (int r = 0; r < op.rep; r++) {
 #pragma unroll
-                    for (int k = 0; k < PPT; k++) montmul_regb<S>(a[k], a[k], p.n, p.n0inv);
+                    for (int k = 0; k < PPT; k++) small_montmul<S>(a[k], a[k], p.n, p.n0inv);
                 }
             } else {
                 uint32_t b[PPT][S];
@@ -259,7 +269,7 @@ modexp_small_kernel(const __grid_constant__ ModexpParams<S> p) {
                 }
                 for (int r = 0; r < op.rep; r++) {
 #pragma unroll
-                    for (int k = 0; k < PPT; k++) montmul_regb<S>(a[k], b[k], p.n, p.n0inv);
+                    for (int k = 0; k < PPT; k++) small_montmul<S>(a[k], b[k], p.n, p.n0inv);
                 }
             }
             if (op.flags & RSA_F_STORE) {

@@ -133,6 +133,54 @@ __device__ __forceinline__ void mont_finish(uint32_t (&a)[S], uint32_t (&X)[S], 
     for (int k = 0; k < S; k++) a[k] = (X[k] & keep) | (a[k] & ~keep);
 }
 
+// 2-limb Montgomery multiply by product scanning (S = 2, R = 2^64): columns 0..2
+// of T = A B + m N accumulate in a 3-word window (c_k, c_k+1, c_k+2); m_0 and
+// m_1 are taken when their column is complete.  Same result as montmul_regb<2>
+// (A B R^-1 mod n, canonical for A < R, B < n) in fewer instructions than the
+// two-step CIOS, whose odd/even split is pointless at S = 2.
+__device__ __forceinline__ void montmul2_ps(uint32_t (&a)[2], const uint32_t (&b)[2], const uint32_t* __restrict__ n,
+                                            uint32_t n0inv) {
+    const uint32_t a0 = a[0], a1 = a[1], b0 = b[0], b1 = b[1], n0 = n[0], n1 = n[1];
+    uint32_t c0, c1, c2, c3, c4, m0, m1;
+    // column 0: a0 b0 + m0 n0 (low word becomes 0)
+    asm("mul.lo.u32 %0, %2, %3;\n\t"
+        "mul.hi.u32 %1, %2, %3;" : "=r"(c0), "=r"(c1) : "r"(a0), "r"(b0));
+    m0 = c0 * n0inv;
+    asm("mad.lo.cc.u32 %0, %3, %4, %0;\n\t"
+        "madc.hi.cc.u32 %1, %3, %4, %1;\n\t"
+        "addc.u32 %2, 0, 0;" : "+r"(c0), "+r"(c1), "=r"(c2) : "r"(m0), "r"(n0));
+    // column 1: a0 b1 + a1 b0 + m0 n1, then m1 n0
+    asm("mad.lo.cc.u32 %0, %3, %4, %0;\n\t"
+        "madc.hi.cc.u32 %1, %3, %4, %1;\n\t"
+        "addc.u32 %2, 0, 0;\n\t"
+        "mad.lo.cc.u32 %0, %5, %6, %0;\n\t"
+        "madc.hi.cc.u32 %1, %5, %6, %1;\n\t"
+        "addc.u32 %2, %2, 0;\n\t"
+        "mad.lo.cc.u32 %0, %7, %8, %0;\n\t"
+        "madc.hi.cc.u32 %1, %7, %8, %1;\n\t"
+        "addc.u32 %2, %2, 0;"
+        : "+r"(c1), "+r"(c2), "=r"(c3) : "r"(a0), "r"(b1), "r"(a1), "r"(b0), "r"(m0), "r"(n1));
+    m1 = c1 * n0inv;
+    asm("mad.lo.cc.u32 %0, %3, %4, %0;\n\t"
+        "madc.hi.cc.u32 %1, %3, %4, %1;\n\t"
+        "addc.u32 %2, %2, 0;" : "+r"(c1), "+r"(c2), "+r"(c3) : "r"(m1), "r"(n0));
+    // column 2: a1 b1 + m1 n1 -> result (c4 : c3 : c2) < 2n
+    asm("mad.lo.cc.u32 %0, %3, %4, %0;\n\t"
+        "madc.hi.cc.u32 %1, %3, %4, %1;\n\t"
+        "addc.u32 %2, 0, 0;\n\t"
+        "mad.lo.cc.u32 %0, %5, %6, %0;\n\t"
+        "madc.hi.cc.u32 %1, %5, %6, %1;\n\t"
+        "addc.u32 %2, %2, 0;"
+        : "+r"(c2), "+r"(c3), "=r"(c4) : "r"(a1), "r"(b1), "r"(m1), "r"(n1));
+    // conditional subtraction
+    uint32_t d0, d1, keep;
+    asm("sub.cc.u32 %0, %3, %5;\n\t"
+        "subc.cc.u32 %1, %4, %6;\n\t"
+        "subc.u32 %2, %7, 0;" : "=r"(d0), "=r"(d1), "=r"(keep) : "r"(c2), "r"(c3), "r"(n0), "r"(n1), "r"(c4));
+    a[0] = keep ? c2 : d0;
+    a[1] = keep ? c3 : d1;
+}
+
 template <int S> struct BVec;
 template <> struct BVec<2> { typedef uint2 T; static constexpr int G = 2; };
 template <int S> struct BVec { typedef uint4 T; static constexpr int G = 4; };

@@ -344,3 +344,65 @@ def test_square_fused_columns(S):
     for A in [0, 1, (1 << (32 * S)) - 1] + [rnd.getrandbits(32 * S) for _ in range(50)]:
         T = square_fused_columns(L(A, S), S)
         assert sum(v << (32 * k) for k, v in enumerate(T)) == A * A
+
+
+# ---------------------------------------------------------------------------
+# montmul2_ps (mont.cuh): the S = 2 product-scanning Montgomery multiply used by
+# the small-width kernel, modelled instruction by instruction (mad.lo.cc takes
+# no carry in, madc.* / addc do).
+
+def montmul2_ps_model(a, b, n):
+    a0, a1 = a & M32, a >> 32
+    b0, b1 = b & M32, b >> 32
+    n0, n1 = n & M32, n >> 32
+    n0inv = (-pow(n0, -1, 2**32)) % 2**32
+    cc = CC()
+    p = a0 * b0
+    c0, c1 = p & M32, p >> 32
+    m0 = (c0 * n0inv) & M32
+    c0 = cc.mad_lo_cc(m0, n0, c0)
+    assert c0 == 0
+    c = cc.c; c1 = cc.mad_hi_cc(m0, n0, c1, c)
+    c2 = cc.c
+    # column 1
+    c1 = cc.mad_lo_cc(a0, b1, c1)
+    c = cc.c; c2 = cc.mad_hi_cc(a0, b1, c2, c)
+    c3 = cc.c
+    c1 = cc.mad_lo_cc(a1, b0, c1)
+    c = cc.c; c2 = cc.mad_hi_cc(a1, b0, c2, c)
+    c3 = c3 + cc.c
+    c1 = cc.mad_lo_cc(m0, n1, c1)
+    c = cc.c; c2 = cc.mad_hi_cc(m0, n1, c2, c)
+    c3 = c3 + cc.c
+    m1 = (c1 * n0inv) & M32
+    c1 = cc.mad_lo_cc(m1, n0, c1)
+    assert c1 == 0
+    c = cc.c; c2 = cc.mad_hi_cc(m1, n0, c2, c)
+    c3 = c3 + cc.c
+    assert c3 < 2**32
+    # column 2
+    c2 = cc.mad_lo_cc(a1, b1, c2)
+    c = cc.c; c3 = cc.mad_hi_cc(a1, b1, c3, c)
+    c4 = cc.c
+    c2 = cc.mad_lo_cc(m1, n1, c2)
+    c = cc.c; c3 = cc.mad_hi_cc(m1, n1, c3, c)
+    c4 = c4 + cc.c
+    assert c4 <= 1
+    # conditional subtraction: borrow chain, keep = c4 - borrow
+    d = (c3 << 32 | c2) - n
+    borrow = 1 if d < 0 else 0
+    keep = (c4 - borrow) & M32
+    return (c3 << 32 | c2) if keep else d & (2**64 - 1)
+
+
+def test_montmul2_ps_model():
+    rng = random.Random(14071465)
+    R = 2**64
+    mods = [3, 17947, 513581, 2**32 - 5, 2**32 + 15, 2**63 + 29, 2**64 - 59, 2**64 - 1]
+    mods += [rng.randrange(3, 2**64) | 1 for _ in range(200)]
+    for n in mods:
+        rinv = pow(R, -1, n)
+        cases = [(R - 1, n - 1), (0, n - 1), (R - 1, 0), (1, 1), (n - 1, n - 1)]
+        cases += [(rng.randrange(R), rng.randrange(n)) for _ in range(50)]
+        for a, b in cases:
+            assert montmul2_ps_model(a, b, n) == a * b * rinv % n, (a, b, n)
