@@ -46,9 +46,11 @@ struct NSharedT {
 // in place otherwise) -- helpers for the chains below.
 template <int S, class NShared>
 __device__ __forceinline__ void red_odd_inplace(uint32_t (&Y)[S], uint32_t& hi, uint32_t m, const NShared& n) {
+    uint4 nxt = n.odd(0);
 #pragma unroll
     for (int q = 0; q < S / 8; q++) {
-        const uint4 v = n.odd(q);
+        const uint4 v = nxt;                   // prefetched one group ahead (LDS latency)
+        if (q + 1 < S / 8) nxt = n.odd(q + 1);
         const int j = 8 * q + 1;
         if (q == 0) mad_lo_cc(Y[0], v.x, m, Y[0]);
         else madc_lo_cc(Y[j - 1], v.x, m, Y[j - 1]);
@@ -66,9 +68,11 @@ __device__ __forceinline__ void red_odd_inplace(uint32_t (&Y)[S], uint32_t& hi, 
 template <int S, class NShared>
 __device__ __forceinline__ void red_even_inplace(uint32_t (&X)[S], uint32_t (&Y)[S], uint32_t& hi, uint32_t m,
                                                  const NShared& n) {
+    uint4 nxt = n.even(0);
 #pragma unroll
     for (int q = 0; q < S / 8; q++) {
-        const uint4 v = n.even(q);
+        const uint4 v = nxt;
+        if (q + 1 < S / 8) nxt = n.even(q + 1);
         const int j = 8 * q;
         if (q == 0) mad_lo_cc(X[0], v.x, m, X[0]);
         else madc_lo_cc(X[j], v.x, m, X[j]);
@@ -115,11 +119,13 @@ __device__ __forceinline__ void cios_step_sm(uint32_t (&X)[S], uint32_t (&Y)[S],
 template <int S, class NShared>
 __device__ __forceinline__ void red_step_sm(uint32_t (&X)[S], uint32_t (&Y)[S], uint32_t& hi, const NShared& n,
                                             uint32_t n0inv) {
+    uint4 nxt = n.odd(0);
     add_cc(X[0], X[0], Y[1]);
     const uint32_t m = X[0] * n0inv;
 #pragma unroll
     for (int q = 0; q < S / 8; q++) {
-        const uint4 v = n.odd(q);
+        const uint4 v = nxt;
+        if (q + 1 < S / 8) nxt = n.odd(q + 1);
         const int j = 8 * q + 1;
         madc_lo_cc(Y[j - 1], v.x, m, Y[j + 1]);
         madc_hi_cc(Y[j], v.x, m, Y[j + 2]);
