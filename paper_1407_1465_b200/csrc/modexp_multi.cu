@@ -17,6 +17,7 @@
 //           x^(2^j) == n - 1, j < r;  out[i] = 1 (probable prime) / 0.
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <type_traits>
 
 #include "mont_multi.cuh"
 
@@ -38,9 +39,19 @@ struct MultiParams {
 };
 
 template <int S>
+#ifndef RSA_MMINB32
+#define RSA_MMINB32 2
+#endif
+#ifndef RSA_MMINB16
+#define RSA_MMINB16 4
+#endif
+#ifndef RSA_MULTI_NREG_MAX
+#define RSA_MULTI_NREG_MAX 32
+#endif
 struct MCfg {
     static constexpr int BLOCK = (S >= 64) ? 256 : 128;
-    static constexpr int MINB = (S >= 64) ? 1 : (S >= 32 ? 2 : 4);
+    static constexpr bool NREG = (S <= RSA_MULTI_NREG_MAX);   // n in registers (else shared memory)
+    static constexpr int MINB = (S >= 64) ? 1 : (S >= 32 ? RSA_MMINB32 : RSA_MMINB16);
 };
 
 // w bits of a packet's exponent at bit position pos (bits beyond the packet are 0)
@@ -58,11 +69,16 @@ modexp_multi_kernel(const __grid_constant__ MultiParams p) {
     constexpr int NQ = S / 8;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     constexpr int stride = MCfg<S>::BLOCK;       // launched with exactly this block size
-    using NS = NSharedT<stride>;
+    constexpr bool NREG = MCfg<S>::NREG;
+    using NS = std::conditional_t<NREG, NRegsT<S, stride>, NSharedT<stride>>;
     uint4* const bslot = reinterpret_cast<uint4*>(smem_raw) + threadIdx.x;
     uint4* const nodd = reinterpret_cast<uint4*>(smem_raw) + NG * stride + threadIdx.x;
     uint4* const neven = nodd + NQ * stride;
-    const NS nsh{nodd, neven};
+    uint32_t nreg[S];
+    const NS nsh = [&] {
+        if constexpr (NREG) return NS{nreg};
+        else return NS{nodd, neven};
+    }();
     const unsigned gtid = blockIdx.x * blockDim.x + threadIdx.x;
     const unsigned nthr = gridDim.x * blockDim.x;
     const int w = p.window;
@@ -97,10 +113,15 @@ modexp_multi_kernel(const __grid_constant__ MultiParams p) {
         // ---- the modulus into this thread's smem slot (odd / even limbs)
 #pragma unroll
         for (int k = 0; k < S; k++) a[k] = (k < p.s_io) ? __ldg(nsrc + k) : 0u;
+        if constexpr (NREG) {
 #pragma unroll
-        for (int q = 0; q < NQ; q++) {
-            nodd[q * stride] = make_uint4(a[8 * q + 1], a[8 * q + 3], a[8 * q + 5], a[8 * q + 7]);
-            neven[q * stride] = make_uint4(a[8 * q], a[8 * q + 2], a[8 * q + 4], a[8 * q + 6]);
+            for (int k = 0; k < S; k++) nreg[k] = a[k];
+        } else {
+#pragma unroll
+            for (int q = 0; q < NQ; q++) {
+                nodd[q * stride] = make_uint4(a[8 * q + 1], a[8 * q + 3], a[8 * q + 5], a[8 * q + 7]);
+                neven[q * stride] = make_uint4(a[8 * q], a[8 * q + 2], a[8 * q + 4], a[8 * q + 6]);
+            }
         }
         bool small = a[0] < 3;
 #pragma unroll

@@ -42,6 +42,22 @@ struct NSharedT {
     }
 };
 
+// Per-thread n held in registers (classes small enough to afford S more
+// registers): same interface as NSharedT, no shared-memory traffic for n.
+// STRIDE is still the b slot stride of montmul_sm.
+template <int S, int STRIDE>
+struct NRegsT {
+    const uint32_t (&n)[S];
+    static constexpr int stride = STRIDE;
+    __device__ __forceinline__ uint4 odd(int q) const {
+        return make_uint4(n[8 * q + 1], n[8 * q + 3], n[8 * q + 5], n[8 * q + 7]);
+    }
+    __device__ __forceinline__ uint4 even(int q) const {
+        return make_uint4(n[8 * q], n[8 * q + 2], n[8 * q + 4], n[8 * q + 6]);
+    }
+    __device__ __forceinline__ uint32_t limb(int j) const { return n[j]; }
+};
+
 // T += m * n (odd limbs into Y, shifted as in the CIOS step when `rshift`;
 // in place otherwise) -- helpers for the chains below.
 template <int S, class NShared>
