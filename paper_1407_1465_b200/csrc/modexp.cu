@@ -74,25 +74,30 @@ modexp_kernel(const __grid_constant__ ModexpParams<S> p) {
         const unsigned long long pkt = valid ? pkt0 : p.count - 1;
         uint32_t a[S];
         int io_status = 0;
-        // a2: load the packet (packet-major at the boundary), zero padded
+        // a2: load the packet (packet-major at the boundary), zero padded; also
+        // the b operand of RSA_OP_MULX (this thread's packet is read before its
+        // own store, so the read-only path stays valid in place)
         const uint32_t* src = p.base + pkt * (unsigned long long)p.s_io;
-        if constexpr (IO == 1) {
-            const uchar2 ch = reinterpret_cast<const uchar2*>(p.base)[pkt];
-            const uint32_t hi = (uint32_t)ch.x - 'a', lo = (uint32_t)ch.y - 'a';
-            if (hi > 25u || lo > 25u) io_status = -7;
+        auto load_input = [&](uint32_t (&x)[S], int& st) {
+            if constexpr (IO == 1) {
+                const uchar2 ch = reinterpret_cast<const uchar2*>(p.base)[pkt];
+                const uint32_t hi = (uint32_t)ch.x - 'a', lo = (uint32_t)ch.y - 'a';
+                if (hi > 25u || lo > 25u) st = -7;
 #pragma unroll
-            for (int k = 0; k < S; k++) a[k] = 0u;
-            a[0] = (io_status ? 0u : hi * 100u + lo);
-        } else if (p.s_io == S && (S % 4) == 0) {
+                for (int k = 0; k < S; k++) x[k] = 0u;
+                x[0] = (st ? 0u : hi * 100u + lo);
+            } else if (p.s_io == S && (S % 4) == 0) {
 #pragma unroll
-            for (int k = 0; k < S; k += 4) {
-                const uint4 v = __ldg(reinterpret_cast<const uint4*>(src + k));
-                a[k] = v.x; a[k + 1] = v.y; a[k + 2] = v.z; a[k + 3] = v.w;
+                for (int k = 0; k < S; k += 4) {
+                    const uint4 v = __ldg(reinterpret_cast<const uint4*>(src + k));
+                    x[k] = v.x; x[k + 1] = v.y; x[k + 2] = v.z; x[k + 3] = v.w;
+                }
+            } else {
+#pragma unroll
+                for (int k = 0; k < S; k++) x[k] = (k < p.s_io) ? __ldg(src + k) : 0u;
             }
-        } else {
-#pragma unroll
-            for (int k = 0; k < S; k++) a[k] = (k < p.s_io) ? __ldg(src + k) : 0u;
-        }
+        };
+        load_input(a, io_status);
 
         for (int i = 0; i < p.nops; i++) {
             const RsaOp op = p.ops[i];
@@ -120,6 +125,16 @@ modexp_kernel(const __grid_constant__ ModexpParams<S> p) {
                     for (int g = 0; g < NG; g++) {
                         V v; v.x = p.r2[G * g]; v.y = p.r2[G * g + 1];
                         if constexpr (G == 4) { v.z = p.r2[G * g + 2]; v.w = p.r2[G * g + 3]; }
+                        bslot[g * stride] = v;
+                    }
+                } else if (op.kind == RSA_OP_MULX) {
+                    uint32_t x[S];
+                    int st = 0;
+                    load_input(x, st);
+#pragma unroll
+                    for (int g = 0; g < NG; g++) {
+                        V v; v.x = x[G * g]; v.y = x[G * g + 1];
+                        if constexpr (G == 4) { v.z = x[G * g + 2]; v.w = x[G * g + 3]; }
                         bslot[g * stride] = v;
                     }
                 } else {  // RSA_OP_ONE
@@ -219,24 +234,28 @@ modexp_small_kernel(const __grid_constant__ ModexpParams<S> p) {
         unsigned long long pkt[PPT];
         bool valid[PPT];
         int io_status[PPT];
+        // packet k's input (also the b operand of RSA_OP_MULX)
+        auto load_input = [&](unsigned long long pk, uint32_t (&x)[S], int& st) {
+            if constexpr (IO == 1) {
+                const uchar2 ch = reinterpret_cast<const uchar2*>(p.base)[pk];
+                const uint32_t hi = (uint32_t)ch.x - 'a', lo = (uint32_t)ch.y - 'a';
+                if (hi > 25u || lo > 25u) st = -7;
+#pragma unroll
+                for (int j = 0; j < S; j++) x[j] = 0u;
+                x[0] = (st ? 0u : hi * 100u + lo);
+            } else {
+                const uint32_t* src = p.base + pk * (unsigned long long)p.s_io;
+#pragma unroll
+                for (int j = 0; j < S; j++) x[j] = (j < p.s_io) ? __ldg(src + j) : 0u;
+            }
+        };
 #pragma unroll
         for (int k = 0; k < PPT; k++) {
             const unsigned long long p0 = t * nvs + (unsigned long long)k * nthr + gtid;
             valid[k] = p0 < p.count;
             pkt[k] = valid[k] ? p0 : p.count - 1;
             io_status[k] = 0;
-            if constexpr (IO == 1) {
-                const uchar2 ch = reinterpret_cast<const uchar2*>(p.base)[pkt[k]];
-                const uint32_t hi = (uint32_t)ch.x - 'a', lo = (uint32_t)ch.y - 'a';
-                if (hi > 25u || lo > 25u) io_status[k] = -7;
-#pragma unroll
-                for (int j = 0; j < S; j++) a[k][j] = 0u;
-                a[k][0] = (io_status[k] ? 0u : hi * 100u + lo);
-            } else {
-                const uint32_t* src = p.base + pkt[k] * (unsigned long long)p.s_io;
-#pragma unroll
-                for (int j = 0; j < S; j++) a[k][j] = (j < p.s_io) ? __ldg(src + j) : 0u;
-            }
+            load_input(pkt[k], a[k], io_status[k]);
         }
         for (int i = 0; i < p.nops; i++) {
             const RsaOp op = p.ops[i];
@@ -261,6 +280,9 @@ modexp_small_kernel(const __grid_constant__ ModexpParams<S> p) {
                         const V v = table[(size_t)op.bidx * nvs + (size_t)k * nthr + gtid];
                         b[k][0] = v.x; b[k][1] = v.y;
                         if constexpr (S == 4) { b[k][2] = v.z; b[k][3] = v.w; }
+                    } else if (op.kind == RSA_OP_MULX) {
+                        int st = 0;
+                        load_input(pkt[k], b[k], st);
                     } else {
 #pragma unroll
                         for (int j = 0; j < S; j++)
@@ -383,6 +405,15 @@ modexp_pair_kernel(const __grid_constant__ ModexpParams<S> p) {
                     for (int g = 0; g < NGL; g++) {
                         const int o = half * L + 4 * g;
                         bslot[(half * NGL + g) * ppb] = make_uint4(p.r2[o], p.r2[o + 1], p.r2[o + 2], p.r2[o + 3]);
+                    }
+                } else if (op.kind == RSA_OP_MULX) {          // this lane's half of the raw input
+#pragma unroll
+                    for (int g = 0; g < NGL; g++) {
+                        const int o = half * L + 4 * g;
+                        uint32_t x[4];
+#pragma unroll
+                        for (int k = 0; k < 4; k++) x[k] = (o + k < p.s_io) ? __ldg(src + o + k) : 0u;
+                        bslot[(half * NGL + g) * ppb] = make_uint4(x[0], x[1], x[2], x[3]);
                     }
                 } else {
 #pragma unroll
@@ -544,6 +575,15 @@ modexp_group_kernel(const __grid_constant__ ModexpParams<S> p) {
                     for (int g = 0; g < NGL; g++) {
                         const int o = lig * L + 4 * g;
                         bslot[(lig * NGL + g) * ppb] = make_uint4(p.r2[o], p.r2[o + 1], p.r2[o + 2], p.r2[o + 3]);
+                    }
+                } else if (op.kind == RSA_OP_MULX) {          // this lane's part of the raw input
+#pragma unroll
+                    for (int g = 0; g < NGL; g++) {
+                        const int o = lig * L + 4 * g;
+                        uint32_t x[4];
+#pragma unroll
+                        for (int k = 0; k < 4; k++) x[k] = (o + k < p.s_io) ? __ldg(src + o + k) : 0u;
+                        bslot[(lig * NGL + g) * ppb] = make_uint4(x[0], x[1], x[2], x[3]);
                     }
                 } else {
 #pragma unroll

@@ -25,6 +25,11 @@ enum RsaOpKind : uint8_t {
     RSA_OP_MUL = 1,    // A <- A * T[bidx] * R^-1   (T = per-thread window table)
     RSA_OP_R2 = 2,     // A <- A * (R^2 mod n) * R^-1   (to Montgomery form)
     RSA_OP_ONE = 3,    // A <- A * 1 * R^-1              (from Montgomery form)
+    RSA_OP_MULX = 4,   // A <- A * x * R^-1, x = the packet's input as given (not in
+                       // Montgomery form): the last multiply by g and the conversion
+                       // from Montgomery form in one.  A < n and x < R keep
+                       // A x + m n < 2 n R, so one conditional subtraction suffices
+                       // for any input x (also x >= n).
 };
 
 enum RsaOpFlags : uint8_t {

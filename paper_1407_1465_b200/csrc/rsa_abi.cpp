@@ -147,8 +147,16 @@ static bool build_ops(const BN& e, int w, int cap, std::vector<RsaOp>* ops, int*
         }
         if (win[k].val >= 0) push(RSA_OP_MUL, 1, 0, win[k].val >> 1, 0, 0);
     }
-    // from Montgomery form (+ the initial load if the scan had one window)
-    push(RSA_OP_ONE, 1, pending_load ? RSA_F_LOADA : 0, 0, first, 0);
+    // from Montgomery form (+ the initial load if the scan had one window).  When
+    // the scan ends with a multiply by g itself (last digit 1, e.g. every odd
+    // public exponent at w = 1), that multiply takes the raw input x instead of
+    // g R, which lands outside Montgomery form directly: one montmul fewer.
+    if (!pending_load && ops->back().kind == RSA_OP_MUL && ops->back().bidx == 0 && ops->back().flags == 0 &&
+        ops->back().rep == 1) {
+        ops->back().kind = RSA_OP_MULX;
+    } else {
+        push(RSA_OP_ONE, 1, pending_load ? RSA_F_LOADA : 0, 0, first, 0);
+    }
     return (int)ops->size() <= cap;
 }
 

@@ -19,8 +19,11 @@ sys.path.insert(0, %r)
 import oracle, workload, paper_1407_1465_b200 as R
 k = workload.key(sys.argv[1]); nb = k["nbits"]; s = workload.limbs_needed(nb)
 m = workload.packets(int(sys.argv[2]), nb, n=k["n"], config_id=21)
+R_ = 1 << (32 * s)                      # inputs at and above n as well (the call is total)
+edge = [v for v in (k["n"], k["n"] + 1, 2 * k["n"] - 1, R_ - 1, R_ - 2) if v < R_]
+m = np.concatenate([m, workload.ints_to_rows(edge, s)])
 t = torch.from_numpy(m.view(np.int32)).cuda()
-for e in (k["e"], k["d"]):
+for e in (k["e"], k["d"], 3):
     got = R.rsa_modexp_batch(t, e, k["n"], nb).cpu().numpy().view(np.uint32)
     assert np.array_equal(got, oracle.modexp_batch(m, e, k["n"])[:, :s]), e
 print("shape ok")
