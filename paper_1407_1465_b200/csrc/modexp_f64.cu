@@ -1,0 +1,191 @@
+// modexp_f64.cu -- batched modular exponentiation on the FP64 pipe (sm_100a).
+//
+// Same contract and operation list as modexp_kernel (modexp.cu): out[i] =
+// base[i]^exp mod n for every packet (sec. 2; PAPER.md:65,
+// sec. 3.3), one thread per packet, the shared exponent's op list executed
+// warp-uniformly.  The Montgomery multiply is mont_f64.cuh: 52-bit digits in
+// doubles, products split exactly by DFMA.RZ, column sums in 64-bit integers.
+//
+// Per thread: A (ND doubles) and the CIOS accumulator (ND 64-bit columns) in
+// registers; the b operand streams from this thread's shared-memory slot
+// (digit-major across the block: conflict-free LDS.64); n's digits are
+// constant-bank operands of the DFMAs.  The window table holds entries as
+// digit pairs (double2), entry-major then digit-pair-major across the grid's
+// threads (coalesced).  Intermediates stay < 2n (R = 2^(52 ND) > 4n), and one
+// subtraction canonicalises the result before the store.
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "mont_f64.cuh"
+#include "plan.h"
+
+namespace rsa_b200 {
+
+template <int S>
+struct F64Cfg {
+    static constexpr int ND = rsa_f64_digits(S);
+    // one 256-thread CTA per SM and a barrier per Montgomery op keep the SM's
+    // 8 warps on the same code lines: the unrolled squaring is ~80 KB of SASS,
+    // and drifting warps stall on instruction fetch (ncu: no_instruction).
+#ifndef RSA_F64_BLOCK
+#define RSA_F64_BLOCK 256
+#endif
+    static constexpr int BLOCK = RSA_F64_BLOCK;
+    static constexpr int MINB = 256 / RSA_F64_BLOCK;
+    static constexpr bool LOCKSTEP = (RSA_F64_BLOCK == 256);
+#ifndef RSA_F64_SQR
+#define RSA_F64_SQR 1
+#endif
+    static constexpr bool SQR = RSA_F64_SQR;     // dedicated squaring (montsqr) vs montmul(a, a)
+};
+
+template <int S>
+__global__ void __launch_bounds__(F64Cfg<S>::BLOCK, F64Cfg<S>::MINB)
+modexp_f64_kernel(const __grid_constant__ ModexpF64Params<S> p) {
+    constexpr int ND = F64Cfg<S>::ND;
+    constexpr int NP = ND / 2;
+    static_assert(ND % 2 == 0, "digit pairs");
+    extern __shared__ __align__(16) double bsm_raw[];
+    double* const bsm = bsm_raw + threadIdx.x;
+    const int stride = blockDim.x;
+    const unsigned gtid = blockIdx.x * blockDim.x + threadIdx.x;
+    const unsigned nthr = gridDim.x * blockDim.x;
+    double2* const table = reinterpret_cast<double2*>(p.ip.table);
+    const ModexpParams<S>& ip = p.ip;
+    // n's digits, one shared copy per block (read by the volatile pair loads
+    // of mont_f64.cuh)
+    __shared__ __align__(16) double nds[ND];
+    for (int k = threadIdx.x; k < ND; k += blockDim.x) nds[k] = p.nd[k];
+    __syncthreads();
+
+    // every thread runs the same number of trips (uniform barriers); an
+    // out-of-range trip recomputes the last packet and skips the store
+    const unsigned long long trips = (ip.count + nthr - 1) / nthr;
+    for (unsigned long long tr = 0; tr < trips; tr++) {
+        const unsigned long long pkt0 = gtid + tr * nthr;
+        const bool valid = pkt0 < ip.count;
+        const unsigned long long pkt = valid ? pkt0 : ip.count - 1;
+        const uint32_t* src = ip.base + pkt * (unsigned long long)ip.s_io;
+        auto load_input = [&](double (&x)[ND]) {
+            uint32_t l[S];
+            if (ip.s_io == S) {
+#pragma unroll
+                for (int k = 0; k < S; k += 4) {
+                    const uint4 v = __ldg(reinterpret_cast<const uint4*>(src + k));
+                    l[k] = v.x; l[k + 1] = v.y; l[k + 2] = v.z; l[k + 3] = v.w;
+                }
+            } else {
+#pragma unroll
+                for (int k = 0; k < S; k++) l[k] = (k < ip.s_io) ? __ldg(src + k) : 0u;
+            }
+            f64::limbs_to_digits<S, ND>(l, x);
+        };
+        double a[ND];
+        uint64_t t[ND];
+        load_input(a);
+        auto from_smem = [&](int i) { return bsm[i * stride]; };
+
+        for (int i = 0; i < ip.nops; i++) {
+            const RsaOp op = ip.ops[i];
+            if (op.flags & RSA_F_LOADA) {
+#pragma unroll
+                for (int g = 0; g < NP; g++) {
+                    const double2 v = table[((size_t)op.lidx * NP + g) * nthr + gtid];
+                    a[2 * g] = v.x; a[2 * g + 1] = v.y;
+                }
+            }
+            for (int r = 0; r < op.rep; r++) {
+                if constexpr (F64Cfg<S>::LOCKSTEP) __syncthreads();
+                // stage the b operand in this thread's slot; one montmul call site
+                // keeps the kernel's code (and its register allocation) single
+                if (op.kind == RSA_OP_SQR) {
+                    if constexpr (F64Cfg<S>::SQR) {
+                        // T_high of the square goes to this thread's slot
+                        f64::montsqr<ND>(a, nds, p.np52, p.c104, t, reinterpret_cast<uint64_t*>(bsm), stride);
+                        continue;
+                    }
+#pragma unroll
+                    for (int k = 0; k < ND; k++) bsm[k * stride] = a[k];
+                } else if (op.kind == RSA_OP_MUL) {
+#pragma unroll
+                    for (int g = 0; g < NP; g++) {
+                        const double2 v = table[((size_t)op.bidx * NP + g) * nthr + gtid];
+                        bsm[(2 * g) * stride] = v.x;
+                        bsm[(2 * g + 1) * stride] = v.y;
+                    }
+                } else if (op.kind == RSA_OP_R2) {
+#pragma unroll
+                    for (int k = 0; k < ND; k++) bsm[k * stride] = p.r2d[k];
+                } else if (op.kind == RSA_OP_MULX) {
+                    double x[ND];
+                    load_input(x);
+#pragma unroll
+                    for (int k = 0; k < ND; k++) bsm[k * stride] = x[k];
+                } else {  // RSA_OP_ONE
+#pragma unroll
+                    for (int k = 0; k < ND; k++) bsm[k * stride] = (k == 0) ? 1.0 : 0.0;
+                }
+                f64::montmul<ND>(a, from_smem, nds, p.np52, p.c104, t);
+            }
+            if (op.flags & RSA_F_STORE) {
+#pragma unroll
+                for (int g = 0; g < NP; g++)
+                    table[((size_t)op.sidx * NP + g) * nthr + gtid] = make_double2(a[2 * g], a[2 * g + 1]);
+            }
+        }
+
+        // the last op (RSA_OP_ONE or RSA_OP_MULX) left the digits in t, < 2n
+        f64::canonicalise<ND>(t, reinterpret_cast<const uint64_t*>(p.nu));
+        uint32_t l[S];
+        f64::digits_to_limbs<S, ND>(t, l);
+        uint32_t* dst = ip.out + pkt * (unsigned long long)ip.s_io;
+        if (!valid) {
+        } else if (ip.s_io == S) {
+#pragma unroll
+            for (int k = 0; k < S; k += 4)
+                *reinterpret_cast<uint4*>(dst + k) = make_uint4(l[k], l[k + 1], l[k + 2], l[k + 3]);
+        } else {
+#pragma unroll
+            for (int k = 0; k < S; k++)
+                if (k < ip.s_io) dst[k] = l[k];
+        }
+    }
+}
+
+template <int S>
+static cudaError_t launch_f64(const void* params, int sms, cudaStream_t stream, int* grid_out, int* block_out,
+                              size_t* slots_out, bool query_only) {
+    const int block = F64Cfg<S>::BLOCK;
+    const size_t smem = sizeof(double) * F64Cfg<S>::ND * (F64Cfg<S>::SQR ? 2 : 1) * block;
+    static int occ = -1;
+    if (occ < 0) {
+        cudaError_t e = cudaFuncSetAttribute(modexp_f64_kernel<S>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)smem);
+        if (e != cudaSuccess) return e;
+        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, modexp_f64_kernel<S>, block, smem);
+        if (e != cudaSuccess) return e;
+        if (occ < 1) occ = 1;
+    }
+    int grid = sms * occ;
+    if (grid_out) *grid_out = grid;
+    if (block_out) *block_out = block;
+    if (slots_out) *slots_out = (size_t)grid * block;
+    if (query_only) return cudaSuccess;
+    const ModexpF64Params<S>& prm = *static_cast<const ModexpF64Params<S>*>(params);
+    const unsigned long long need = (prm.ip.count + block - 1) / block;
+    if (need < (unsigned long long)grid) grid = (int)need;
+    modexp_f64_kernel<S><<<grid, block, smem, stream>>>(prm);
+    return cudaGetLastError();
+}
+
+}  // namespace rsa_b200
+
+// host entry points (C++ linkage) used by modexp.cu's dispatch
+cudaError_t rsa_b200_launch_f64(int S, const void* params, int sms, cudaStream_t stream, int* grid, int* block,
+                                size_t* slots, bool query_only) {
+    using namespace rsa_b200;
+    switch (S) {
+    case 64: return launch_f64<64>(params, sms, stream, grid, block, slots, query_only);
+    default: return cudaErrorInvalidValue;
+    }
+}

@@ -1,0 +1,328 @@
+// mont_f64.cuh -- Montgomery multiplication on the FP64 pipe (52-bit digits).
+//
+// Same operation as mont.cuh (Fig 3 "(u*v) mod
+// m", realised by Montgomery reduction), different number
+// representation: numbers are ND digits of D = 52 bits held as doubles, and
+// every 52x52 -> 104-bit digit product is split exactly into its high and low
+// halves by two fused multiply-adds:
+//
+//   h = fma_rz(x, y, 2^104)          = 2^104 + floor(x y / 2^52) 2^52
+//   l = fma_rz(x, y, 2^104 + 2^52 - h) = 2^52 + (x y mod 2^52)        (exact)
+//
+// (the first rounds toward zero inside the binade [2^104, 2^105) whose ulp is
+// 2^52; the second is an integer in [2^52, 2^53) and so exact).  Both results
+// carry their integer in the low 52 bits of their IEEE bit pattern, on top of
+// a constant exponent field (Bh = 0x467 << 52, Bl = 0x433 << 52).  Column sums
+// therefore accumulate the raw bit patterns with 64-bit integer adds (IADD3 +
+// IADD3.X on the ALU pipe); the exponent fields add a known multiple of 2^52
+// per term (mod 2^64), which is subtracted only where a carry is taken.  No
+// carry chains: a column of the CIOS accumulator receives 4 terms < 2^52 per
+// iteration and lives <= ND iterations, so its true value stays < 2^60.
+//
+// Why: on B200 the DFMA pipe issues ~53 results/clk/SM (profiles/
+// r01_imad_peak.jsonl) and one 52x52 product costs 3 FP64 ops (DFMA, DADD,
+// DFMA) -> ~17.7 products x 2704 bit^2 per clk, against ~28 IMAD.WIDE.X
+// products x 1024 bit^2 on the integer pipe: 1.66x the multiply throughput.
+//
+// CIOS (operand scanning) with R = 2^(52 ND), for i = 0 .. ND-1:
+//   T += A b_i ;  q = T_0 n' mod 2^52 ;  T += q n ;  T /= 2^52
+// The division is a register rename folded into the adds: column j of the
+// new T is written from column j+1 of the old one (t[j-1] = t[j] + ...), in
+// place, so a loop iteration needs no moves and no unrolling.
+//
+// Bounds: A, B < 2n and 4n < R give T < 2n (almost-Montgomery: no
+// subtraction inside the exponentiation; the caller canonicalises once at the
+// end).  Pinned on CPU by tests/test_f64_model.py (this header compiled for
+// the host with the rounding mode set to toward-zero).
+#pragma once
+#include <stdint.h>
+
+#ifndef __CUDA_ARCH__
+#include <cmath>
+#include <cstring>
+#endif
+
+namespace rsa_b200 {
+namespace f64 {
+
+constexpr int D = 52;
+constexpr uint64_t M52 = (1ull << 52) - 1;
+constexpr uint64_t BL = 0x433ull << 52;            // bit pattern of 2^52
+constexpr uint64_t BH = 0x467ull << 52;            // bit pattern of 2^104
+constexpr uint64_t BETA = 2 * BL + 2 * BH;         // exponent fields added to an interior column per iteration
+constexpr double C104 = 20282409603651670423947251286016.0;   // 2^104
+constexpr double C2 = 20282409603651674927546878656512.0;     // 2^104 + 2^52
+constexpr double C52 = 4503599627370496.0;                      // 2^52
+
+// digits needed for a Montgomery radix R = 2^(52 ND) > 4n with n < 2^(32 S)
+template <int S> struct Digits { static constexpr int ND = (32 * S + 2 + D - 1) / D; };
+
+__host__ __device__ __forceinline__ uint64_t bits(double x) {
+#ifdef __CUDA_ARCH__
+    return (uint64_t)__double_as_longlong(x);
+#else
+    uint64_t u; memcpy(&u, &x, 8); return u;
+#endif
+}
+__host__ __device__ __forceinline__ double from_bits(uint64_t u) {
+#ifdef __CUDA_ARCH__
+    return __longlong_as_double((long long)u);
+#else
+    double x; memcpy(&x, &u, 8); return x;
+#endif
+}
+// host: the caller runs with fesetround(FE_TOWARDZERO) (the only inexact op)
+__host__ __device__ __forceinline__ double fma_rz(double a, double b, double c) {
+#ifdef __CUDA_ARCH__
+    return __fma_rz(a, b, c);
+#else
+    return std::fma(a, b, c);
+#endif
+}
+__host__ __device__ __forceinline__ double sub_rn(double a, double b) {   // exact where used
+#ifdef __CUDA_ARCH__
+    return __dsub_rn(a, b);
+#else
+    return a - b;
+#endif
+}
+// digits 2g, 2g+1 of n.  On the device nd points to a per-block shared copy
+// and the load is volatile: ptxas may neither hoist the ND digits into
+// registers ahead of the loop (which starves the product schedule) nor fold
+// them into uniform registers (too few: they spill).
+__host__ __device__ __forceinline__ void nd_pair(const double* nd, int g, double& x, double& y) {
+#ifdef __CUDA_ARCH__
+    asm volatile("ld.volatile.shared.v2.f64 {%0, %1}, [%2];"
+                 : "=d"(x), "=d"(y) : "r"((unsigned)__cvta_generic_to_shared(nd + 2 * g)));
+#else
+    x = nd[2 * g];
+    y = nd[2 * g + 1];
+#endif
+}
+
+// integer d < 2^52 -> double (exact)
+__host__ __device__ __forceinline__ double digit_to_double(uint64_t d) { return sub_rn(from_bits(BL | d), C52); }
+
+// x (S little-endian 32-bit limbs) -> ND digits of 52 bits as doubles
+template <int S, int ND>
+__host__ __device__ __forceinline__ void limbs_to_digits(const uint32_t (&x)[S], double (&a)[ND]) {
+#pragma unroll
+    for (int k = 0; k < ND; k++) {
+        const int o = D * k, L = o / 32, sh = o % 32;
+        uint64_t v = 0;
+        if (L < S) v = (uint64_t)x[L] >> sh;
+        if (L + 1 < S) v |= (uint64_t)x[L + 1] << (32 - sh);
+        if (L + 2 < S && 64 - sh < 52) v |= (uint64_t)x[L + 2] << (64 - sh);
+        a[k] = digit_to_double(v & M52);
+    }
+}
+
+// canonical digits (uint64, < 2^52 each, value < 2^(32 S)) -> S limbs
+template <int S, int ND>
+__host__ __device__ __forceinline__ void digits_to_limbs(const uint64_t (&d)[ND], uint32_t (&x)[S]) {
+#pragma unroll
+    for (int m = 0; m < S; m++) {
+        const int o = 32 * m, k = o / D, sh = o % D;
+        uint64_t v = d[k] >> sh;
+        if (k + 1 < ND && D - sh < 32) v |= d[k + 1] << (D - sh);
+        x[m] = (uint32_t)v;
+    }
+}
+
+// A <- A B R^-1 (mod n), R = 2^(52 ND), result < 2n for A, B < 2n.
+// b(i) returns digit i of B as a double; nd: n's digits as doubles (constant
+// bank on the device); np = -n^-1 mod 2^52; c104 = 2^104, passed in from the
+// kernel parameters: as a register operand it leaves the DFMA's constant-bank
+// slot to n's digits (with the immediate 2^104 ptxas hoists all ND digits of
+// n into registers instead, and the product schedule starves).  The result digits are returned
+// normalised both as doubles (a) and as integers (ai, for the final store).
+template <int ND, typename BF>
+__host__ __device__ __forceinline__ void montmul(double (&a)[ND], BF b, const double* __restrict__ nd, uint64_t np,
+                                                 double c104, uint64_t (&t)[ND]) {
+#pragma unroll
+    for (int k = 0; k < ND; k++) t[k] = 0;
+    uint64_t bias0 = 2 * BL;
+    // Software-pipelined like montsqr's reduction: the quotient digit of
+    // iteration i+1 needs only the new column 0 (complete after the j = 1
+    // products) and a_0 b_{i+1}, so it is computed mid-iteration.
+    double bi = b(0);
+    uint64_t hp0, c0;
+    {
+        const double h0 = fma_rz(a[0], bi, C104);
+        const double l0 = fma_rz(a[0], bi, sub_rn(C2, h0));
+        hp0 = bits(h0);
+        c0 = bits(l0);                                   // t[0] = 0
+    }
+    double qd = digit_to_double(((c0 & M52) * np) & M52);
+#ifdef __CUDA_ARCH__
+#pragma unroll 1
+#endif
+    for (int i = 0; i < ND; i++) {
+        const double bn = b(i + 1 < ND ? i + 1 : i);
+        double n0, n1;
+        nd_pair(nd, 0, n0, n1);
+        const double hq0 = fma_rz(qd, n0, c104);
+        const double lq0 = fma_rz(qd, n0, sub_rn(C2, hq0));
+        const uint64_t carry = (c0 + bits(lq0) - bias0) >> D;     // column 0 is 0 mod 2^52
+        const double h1 = fma_rz(a[1], bi, C104);
+        const double l1 = fma_rz(a[1], bi, sub_rn(C2, h1));
+        const double hq1 = fma_rz(qd, n1, c104);
+        const double lq1 = fma_rz(qd, n1, sub_rn(C2, hq1));
+        t[0] = t[1] + bits(l1) + hp0 + bits(lq1) + bits(hq0) + carry;
+        // next iteration's column 0: + a_0 b_{i+1}
+        const double hn = fma_rz(a[0], bn, C104);
+        const double ln = fma_rz(a[0], bn, sub_rn(C2, hn));
+        const uint64_t c0n = t[0] + bits(ln);
+        const double qnext = digit_to_double(((c0n & M52) * np) & M52);
+        uint64_t hp = bits(h1), hqp = bits(hq1);
+#pragma unroll
+        for (int j = 2; j < ND; j++) {
+            const double h = fma_rz(a[j], bi, C104);
+            const double l = fma_rz(a[j], bi, sub_rn(C2, h));
+            t[j - 1] = t[j] + bits(l) + hp;
+            hp = bits(h);
+        }
+#pragma unroll
+        for (int j = 2; j < ND; j++) {
+            double nj = n1;
+            if ((j & 1) == 0) nd_pair(nd, j / 2, nj, n1);
+            const double h = fma_rz(qd, nj, c104);
+            const double l = fma_rz(qd, nj, sub_rn(C2, h));
+            t[j - 1] += bits(l) + hqp;
+            hqp = bits(h);
+        }
+        t[ND - 1] = hp + hqp;
+        c0 = c0n;
+        hp0 = bits(hn);
+        qd = qnext;
+        bi = bn;
+        bias0 += BETA;
+    }
+    // remove the exponent fields and propagate carries: column p now carries
+    // 2 BH + (ND-1-p) BETA (mod 2^64) on top of its true value
+    uint64_t carry = 0;
+#pragma unroll
+    for (int p = 0; p < ND; p++) {
+        const uint64_t v = t[p] - (2 * BH + (uint64_t)(ND - 1 - p) * BETA) + carry;
+        t[p] = v & M52;
+        carry = v >> D;
+        a[p] = digit_to_double(t[p]);
+    }
+}
+
+// A <- A^2 R^-1 (mod n), result < 2n for A < 2n (squarings are ~85% of a
+// full-d exponentiation).  A square has ND (ND+1)/2 distinct digit products
+// instead of ND^2, so this is separated operand scanning (SOS):
+//   1. T = A^2 by product scanning, fully unrolled: column k sums the low
+//      halves of its cross products a_i a_j (i < j, i + j = k) and the high
+//      halves of column k-1's, once; the column is then doubled and the
+//      diagonal a_{k/2}^2 added (one 64-bit shift-add per column, not per
+//      product).  The 2 ND digits of T go to this thread's shared-memory
+//      slot th[k * stride] as they complete (registers hold A and the
+//      in-flight products only), and the low half is reloaded into t.
+//   2. Reduction-only CIOS on t: q = t_0 n' mod 2^52; t = (t + q n) / 2^52,
+//      ND times (loop, not unrolled).
+//   3. t + T_high, normalised: T / R + Q n / R < 4n^2/R + n < 2n.
+template <int ND>
+__host__ __device__ __forceinline__ void montsqr(double (&a)[ND], const double* __restrict__ nd, uint64_t np,
+                                                 double c104, uint64_t (&t)[ND], uint64_t* th, int stride) {
+    // 1. T = A^2
+    uint64_t carry = 0;
+    uint64_t hx[ND], hd = 0;          // high halves pending for the next column (cross, diagonal)
+    int nhx = 0;
+#pragma unroll
+    for (int k = 0; k < 2 * ND; k++) {
+        uint64_t x = 0, xb = 0;       // cross sum (raw patterns) and its exponent fields
+#pragma unroll
+        for (int m = 0; m < ND; m++)
+            if (m < nhx) { x += hx[m]; xb += BH; }
+        int nh = 0;
+#pragma unroll
+        for (int i = 0; i < ND; i++) {
+            const int j = k - i;
+            if (i < j && j < ND) {
+                const double h = fma_rz(a[i], a[j], C104);
+                const double l = fma_rz(a[i], a[j], sub_rn(C2, h));
+                x += bits(l);
+                xb += BL;
+                hx[nh++] = bits(h);
+            }
+        }
+        nhx = nh;
+        uint64_t y = hd, yb = (k > 0 && ((k - 1) & 1) == 0 && (k - 1) / 2 < ND) ? BH : 0;
+        hd = 0;
+        if ((k & 1) == 0 && k / 2 < ND) {
+            const double ai = a[k / 2];
+            const double h = fma_rz(ai, ai, C104);
+            const double l = fma_rz(ai, ai, sub_rn(C2, h));
+            y += bits(l);
+            yb += BL;
+            hd = bits(h);
+        }
+        const uint64_t v = 2 * (x - xb) + (y - yb) + carry;
+        carry = v >> D;
+        th[k * stride] = v & M52;
+    }
+#pragma unroll
+    for (int p = 0; p < ND; p++) t[p] = th[p * stride];
+    // 2. reduce T_low.  Software-pipelined: the new column 0 is complete once
+    // the j = 1 product is in, so the next quotient digit (an IMAD/LOP/DADD
+    // chain) is computed there and overlaps the remaining ND-2 products.
+    uint64_t bias0 = BL;
+    double qd = digit_to_double(((t[0] & M52) * np) & M52);
+#ifdef __CUDA_ARCH__
+#pragma unroll 1
+#endif
+    for (int i = 0; i < ND; i++) {
+        double n0, n1;
+        nd_pair(nd, 0, n0, n1);
+        const double hq0 = fma_rz(qd, n0, c104);
+        const double lq0 = fma_rz(qd, n0, sub_rn(C2, hq0));
+        const uint64_t cr = (t[0] + bits(lq0) - bias0) >> D;   // column 0 is 0 mod 2^52
+        const double hq1 = fma_rz(qd, n1, c104);
+        const double lq1 = fma_rz(qd, n1, sub_rn(C2, hq1));
+        t[0] = t[1] + bits(lq1) + bits(hq0) + cr;
+        const double qnext = digit_to_double(((t[0] & M52) * np) & M52);
+        uint64_t hqp = bits(hq1);
+#pragma unroll
+        for (int j = 2; j < ND; j++) {
+            double nj = n1;
+            if ((j & 1) == 0) nd_pair(nd, j / 2, nj, n1);
+            const double h = fma_rz(qd, nj, c104);
+            const double l = fma_rz(qd, nj, sub_rn(C2, h));
+            t[j - 1] = t[j] + bits(l) + hqp;
+            hqp = bits(h);
+        }
+        t[ND - 1] = hqp;
+        qd = qnext;
+        bias0 += BL + BH;
+    }
+    // 3. + T_high, normalise (column p carries BH + (ND-1-p)(BL+BH))
+    carry = 0;
+#pragma unroll
+    for (int p = 0; p < ND; p++) {
+        const uint64_t v = t[p] - (BH + (uint64_t)(ND - 1 - p) * (BL + BH)) + th[(ND + p) * stride] + carry;
+        t[p] = v & M52;
+        carry = v >> D;
+        a[p] = digit_to_double(t[p]);
+    }
+}
+
+// r <- r - n if r >= n (digits, r < 2n); nu: n's digits as integers
+template <int ND>
+__host__ __device__ __forceinline__ void canonicalise(uint64_t (&r)[ND], const uint64_t* __restrict__ nu) {
+    uint64_t d[ND];
+    int64_t br = 0;
+#pragma unroll
+    for (int p = 0; p < ND; p++) {
+        const int64_t v = (int64_t)r[p] - (int64_t)nu[p] + br;
+        d[p] = (uint64_t)v & M52;
+        br = v >> D;                 // 0 or -1
+    }
+    const bool keep = br < 0;        // r < n
+#pragma unroll
+    for (int p = 0; p < ND; p++) r[p] = keep ? r[p] : d[p];
+}
+
+}  // namespace f64
+}  // namespace rsa_b200

@@ -65,6 +65,21 @@ struct ModexpParams {
     RsaOp ops[rsa_ops_cap(S)];
 };
 
+// FP64-pipe kernel (mont_f64.cuh) for class S: digits of 52 bits, R = 2^(52 ND)
+// with 4n < R.  The integer params come first, so the blob also serves the
+// IMAD kernel of the same class (patch_params casts it to ModexpParams<S>).
+constexpr int rsa_f64_digits(int S) { return (32 * S + 2 + 51) / 52; }
+
+template <int S>
+struct ModexpF64Params {
+    ModexpParams<S> ip;
+    unsigned long long np52;                 // -n^-1 mod 2^52
+    double c104;                             // 2^104 (a runtime value: see mont_f64.cuh montmul)
+    double nd[rsa_f64_digits(S)];            // n, digits as doubles (DFMA constant-bank operands)
+    double r2d[rsa_f64_digits(S)];           // R^2 mod n, R = 2^(52 ND), digits as doubles
+    unsigned long long nu[rsa_f64_digits(S)];  // n, digits as integers (final subtraction)
+};
+
 // host-visible summary of a plan (also exported through the C-ABI)
 struct RsaPlanInfo {
     int width_class;              // S
