@@ -180,8 +180,27 @@ def measured_chain_rate():
     return best
 
 
-def batch_kernel_name(S: int) -> str:
+def measured_dfma_rate():
+    """Best fma.rn.f64 results/clk/SM in the committed microbenchmark
+    (profiles/r01_imad_peak.jsonl), or None."""
+    best = None
+    try:
+        with open(os.path.join(ROOT, "profiles", "r01_imad_peak.jsonl")) as f:
+            for line in f:
+                if line.startswith("{"):
+                    rec = json.loads(line)
+                    v = rec.get("dfma_per_clk_per_sm")
+                    if v is not None:
+                        best = v if best is None or v > best else best
+    except (OSError, ValueError):
+        return None
+    return best
+
+
+def batch_kernel_name(S: int, fp64: bool = False) -> str:
     """The kernel modexp.cu launches for width class S (same env switches)."""
+    if fp64:
+        return f"modexp_f64_kernel<{S}>"
     if S <= 4 and os.environ.get("RSA_B200_SMALL", "1")[:1] != "0":
         return f"modexp_small_kernel<{S}>"
     if S == 64 and os.environ.get("RSA_B200_SHAPE64", "")[:1] == "g":
@@ -399,12 +418,13 @@ def run_ours(args, rank, world, local_rank):
     products = count * plans[dom]["products"]
     achieved = products / (leg_ms[dom] / 1e3) / 1e12
     peak = R_PRODUCTS_PER_CLK_PER_SM * sms * f_max * 1e6 / 1e12
+    fp64 = kind == "batch" and plans[dom].get("fp64_digits", 0) > 0
     roofline = {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "Tprod/s", "frac": achieved / peak,
                 "traffic": ncu_traffic(key_name, legs[dom][0], count),
                 "traffic_unit": "bytes per launch", "algorithmic_bytes": count * s * 4 * 2,
                 "kernel": ({"multi": f"modexp_multi_kernel<{S}>", "mr": f"modexp_multi_kernel<{S}> (MR mode)",
                             "crt": f"2 x modexp_kernel<{S}> + crt_split/combine (half-width CRT legs; products of both)"}.get(
-                    kind, batch_kernel_name(S))) + f" ({legs[dom][0]})",
+                    kind, batch_kernel_name(S, fp64))) + f" ({legs[dom][0]})",
                 "algorithmic": f"{plans[dom]['products']} 32x32->64 limb products/packet "
                                f"({plans[dom]['squarings']} squarings x "
                                f"{'1.5S^2+1.5S' if plans[dom]['sqr_kernel'] else '2S^2+S'} + "
@@ -413,24 +433,47 @@ def run_ours(args, rank, world, local_rank):
                 "peak_basis": f"{R_PRODUCTS_PER_CLK_PER_SM} products/clk/SM (IMAD.WIDE half rate, "
                               f"profiles/r01_imad_peak.jsonl) x {sms} SMs x {f_max:.0f} MHz "
                               f"(MEASURED_PEAKS sm_max_mhz)"}
+    if fp64:
+        # The dominant kernel runs on the FP64 pipe (mont_f64.cuh): its own
+        # roofline is FP64 ops against the measured DFMA issue rate.  The
+        # metric's "% of IMAD peak" (the same limb-product count against the
+        # integer pipe's peak) is kept beside it: above 1 means the path beats
+        # the integer-pipe ceiling.
+        nd = plans[dom]["fp64_digits"]
+        dfma = measured_dfma_rate() or 64.0
+        ops = 3 * count * plans[dom]["digit_products"]
+        f_ach = ops / (leg_ms[dom] / 1e3) / 1e12
+        f_peak = dfma * sms * f_max * 1e6 / 1e12
+        roofline.update({
+            "achieved": f_ach, "peak": f_peak, "unit": "T fp64-op/s", "frac": f_ach / f_peak,
+            "algorithmic": f"{plans[dom]['digit_products']} 52x52-bit digit products/packet x 3 FP64 ops "
+                           f"(DFMA.RZ hi, DADD, DFMA.RZ lo; {plans[dom]['squarings']} squarings x ND(ND+1)/2+ND^2 + "
+                           f"{plans[dom]['montmuls'] - plans[dom]['squarings']} other montmuls x 2ND^2, ND={nd}) "
+                           f"x {count} packets per launch",
+            "peak_basis": f"{dfma:.1f} fma.rn.f64/clk/SM (profiles/r01_imad_peak.jsonl) x {sms} SMs x "
+                          f"{f_max:.0f} MHz (MEASURED_PEAKS sm_max_mhz)",
+            "imad_equiv": {"achieved": achieved, "peak": peak, "unit": "Tprod/s", "frac": achieved / peak,
+                           "basis": "the path's 32x32->64 limb-product count (the metric's '% of IMAD peak') "
+                                    "against 32 products/clk/SM on the integer pipe"}})
     if kind == "batch":
         # the window table is algorithmic state too: every entry written once,
         # read by each window multiply (+ the A loads); per resident thread it is
         # ntab x S limbs, larger than L2 at S = 64 / w = 7, so it streams to DRAM
         pd = plans[dom]
         touches = pd["table_entries"] + (pd["montmuls"] - pd["squarings"] - 2) + 2
-        roofline["algorithmic_table_bytes"] = count * S * 4 * touches
+        entry = 8 * pd["fp64_digits"] if fp64 else S * 4        # 52-bit digits as doubles, or limbs
+        roofline["algorithmic_table_bytes"] = count * entry * touches
         roofline["traffic_note"] = ("DRAM traffic = packet I/O + the per-thread sliding-window table "
-                                    f"({pd['table_entries']} entries x {S * 4} B, {touches} entry reads/writes per "
+                                    f"({pd['table_entries']} entries x {entry} B, {touches} entry reads/writes per "
                                     "packet); compare traffic with algorithmic_bytes + algorithmic_table_bytes")
     chain = measured_chain_rate()
-    if chain:
+    if chain and not fp64:
         # context, not the contract's peak: the best rate the IMAD microbenchmark
         # sustained for dependent IMAD.WIDE.U32.X chains (any occupancy)
         roofline["peak_measured_chain"] = chain * sms * f_max * 1e6 / 1e12
         roofline["frac_of_measured_chain"] = achieved / roofline["peak_measured_chain"]
     if clk and clk.get("sm_mhz"):
-        roofline["frac_at_measured_clock"] = achieved / (R_PRODUCTS_PER_CLK_PER_SM * sms * clk["sm_mhz"] * 1e6 / 1e12)
+        roofline["frac_at_measured_clock"] = roofline["frac"] * f_max / clk["sm_mhz"]
     legs_out = {}
     for j, (label, field) in enumerate(legs):
         legs_out[label] = {"ms": leg_ms[j], "modexp_per_s": world * count / (leg_ms[j] / 1e3),

@@ -23,7 +23,9 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "librsa_b200.so")
+# RSA_B200_LIB: an alternate in-tree build of the same library (kernel A/B
+# measurements only, e.g. paper_1407_1465_b200/librsa_b200_<variant>.so)
+LIB_PATH = os.environ.get("RSA_B200_LIB") or os.path.join(_HERE, "librsa_b200.so")
 
 RSA_OK, RSA_EINVAL, RSA_ERANGE, RSA_EEVEN = 0, -1, -2, -3
 RSA_ENOTPRIME, RSA_EEQUAL, RSA_ENOTCOPRIME = -4, -5, -6
@@ -48,7 +50,8 @@ class RsaPlanInfo(ctypes.Structure):
     _fields_ = [("width_class", ctypes.c_int), ("s_io", ctypes.c_int), ("window", ctypes.c_int),
                 ("table_entries", ctypes.c_int), ("nops", ctypes.c_int), ("montmuls", ctypes.c_longlong),
                 ("squarings", ctypes.c_longlong), ("exp_bits", ctypes.c_int), ("grid", ctypes.c_int),
-                ("block", ctypes.c_int), ("sqr_kernel", ctypes.c_int), ("products", ctypes.c_longlong)]
+                ("block", ctypes.c_int), ("sqr_kernel", ctypes.c_int), ("products", ctypes.c_longlong),
+                ("fp64_digits", ctypes.c_int), ("digit_products", ctypes.c_longlong)]
 
 
 _lib.rsa_strerror.restype = ctypes.c_char_p

@@ -728,17 +728,18 @@ static bool rsa_b200_small() {
     return v == 1;
 }
 
-// 2048-bit class on the FP64 pipe (modexp_f64.cu, mont_f64.cuh) or on the
-// integer pipe (modexp_kernel<64>); RSA_B200_F64=0/1 selects for A/B runs.
+// 1024- and 2048-bit classes on the FP64 pipe (modexp_f64.cu, mont_f64.cuh;
+// default, measured faster: DESIGN.md) or on the integer pipe
+// (modexp_kernel<S>, RSA_B200_F64=0) for A/B runs.
 cudaError_t rsa_b200_launch_f64(int S, const void* params, int sms, cudaStream_t stream, int* grid, int* block,
                                 size_t* slots, bool query_only);
 static bool rsa_b200_f64(int S) {
     static int v = -1;
     if (v < 0) {
         const char* e = getenv("RSA_B200_F64");
-        v = (e && e[0] == '1') ? 1 : 0;
+        v = (e && e[0] == '0') ? 0 : 1;
     }
-    return v == 1 && S == 64 && !rsa_b200_shape64();
+    return v == 1 && ((S == 64 && !rsa_b200_shape64()) || S == 32);
 }
 
 static int rsa_b200_tpi128() {
@@ -758,7 +759,7 @@ static int rsa_b200_tpi128() {
 // executed-product count of rsa_plan_info.
 int rsa_b200_sqr_dedicated(int S) {
     if (S <= 4) return rsa_b200_small() ? 0 : 1;
-    if (S == 64) return (rsa_b200_shape64() || rsa_b200_f64(64)) ? 0 : 1;
+    if (S == 64) return rsa_b200_shape64() ? 0 : 1;   // (the FP64 kernel squares with montsqr too)
     return S <= 64 ? 1 : 0;
 }
 

@@ -21,21 +21,26 @@
 
 namespace rsa_b200 {
 
-template <int S>
-struct F64Cfg {
-    static constexpr int ND = rsa_f64_digits(S);
-    // one 256-thread CTA per SM and a barrier per Montgomery op keep the SM's
-    // 8 warps on the same code lines: the unrolled squaring is ~80 KB of SASS,
-    // and drifting warps stall on instruction fetch (ncu: no_instruction).
-#ifndef RSA_F64_BLOCK
-#define RSA_F64_BLOCK 256
-#endif
-    static constexpr int BLOCK = RSA_F64_BLOCK;
-    static constexpr int MINB = 256 / RSA_F64_BLOCK;
-    static constexpr bool LOCKSTEP = (RSA_F64_BLOCK == 256);
 #ifndef RSA_F64_SQR
 #define RSA_F64_SQR 1
 #endif
+#ifndef RSA_F64_BLOCK
+#define RSA_F64_BLOCK 256
+#endif
+#ifndef RSA_F64_MINB32
+#define RSA_F64_MINB32 4
+#endif
+template <int S>
+struct F64Cfg {
+    static constexpr int ND = rsa_f64_digits(S);
+    // S = 64: one 256-thread CTA per SM and a barrier per Montgomery op keep
+    // the SM's 8 warps on the same code lines: the unrolled squaring is ~80 KB
+    // of SASS, and drifting warps stall on instruction fetch (ncu:
+    // no_instruction).  S = 32 (ND = 20): ~80 registers of state, small code,
+    // several independent CTAs per SM.
+    static constexpr int BLOCK = (S >= 64) ? RSA_F64_BLOCK : 128;
+    static constexpr int MINB = (S >= 64) ? 256 / RSA_F64_BLOCK : RSA_F64_MINB32;
+    static constexpr bool LOCKSTEP = (S >= 64) && (RSA_F64_BLOCK == 256);
     static constexpr bool SQR = RSA_F64_SQR;     // dedicated squaring (montsqr) vs montmul(a, a)
 };
 
@@ -185,6 +190,7 @@ cudaError_t rsa_b200_launch_f64(int S, const void* params, int sms, cudaStream_t
                                 size_t* slots, bool query_only) {
     using namespace rsa_b200;
     switch (S) {
+    case 32: return launch_f64<32>(params, sms, stream, grid, block, slots, query_only);
     case 64: return launch_f64<64>(params, sms, stream, grid, block, slots, query_only);
     default: return cudaErrorInvalidValue;
     }

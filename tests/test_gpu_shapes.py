@@ -1,5 +1,6 @@
 """The alternative kernel shapes kept for measurement ('chosen by
-measurement'): 2048-bit as a 2-lane group (RSA_B200_SHAPE64=group2) and
+measurement'): the 2048-bit class on the integer pipe or the FP64 pipe
+(RSA_B200_F64=0/1), 2048-bit as a 2-lane group (RSA_B200_SHAPE64=group2) and
 4096-bit as a 4-lane group (RSA_B200_TPI128=4), and the thread-per-packet
 kernel for the small widths (RSA_B200_SMALL=0, instead of the multi-packet
 one) stay bit-exact vs the oracle.
@@ -30,7 +31,11 @@ print("shape ok")
 ''' % ROOT
 
 
-@pytest.mark.parametrize("env,key,count", [("RSA_B200_SHAPE64=group2", "rsa2048", 300),
+@pytest.mark.parametrize("env,key,count", [("RSA_B200_F64=0", "rsa2048", 300),
+                                           ("RSA_B200_F64=0", "rsa1536", 300),
+                                           ("RSA_B200_F64=1", "rsa2048", 300),
+                                           ("RSA_B200_F64=1", "rsa1536", 300),
+                                           ("RSA_B200_SHAPE64=group2", "rsa2048", 300),
                                            ("RSA_B200_SHAPE64=group2", "rsa1536", 300),
                                            ("RSA_B200_TPI128=4", "rsa4096", 60),
                                            ("RSA_B200_TPI128=4", "rsa3072", 60),
