@@ -22,7 +22,13 @@ def stale() -> bool:
     return any(os.path.getmtime(d) > t for d in DEPS)
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
+def build(force: bool = False, verbose: bool = False, out: str | None = None) -> str:
+    """Build the library (to `out` for an A/B variant, loaded with RSA_B200_LIB)."""
+    if out:
+        extra = os.environ.get("RSA_B200_NVCC_EXTRA", "").split()
+        subprocess.check_call([NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-shared", "-Xcompiler", "-fPIC",
+                               *extra, "-o", out, *SOURCES])
+        return out
     if not force and not stale():
         return LIB
     extra = os.environ.get("RSA_B200_NVCC_EXTRA", "").split()   # A/B experiments, e.g. -DRSA_SMALL_PPT2=8
@@ -40,4 +46,5 @@ def build(force: bool = False, verbose: bool = False) -> str:
 
 
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv))
+    o = [a.split("=", 1)[1] for a in sys.argv if a.startswith("--out=")]
+    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv, out=o[0] if o else None))

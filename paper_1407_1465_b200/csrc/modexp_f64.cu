@@ -27,6 +27,9 @@ namespace rsa_b200 {
 #ifndef RSA_F64_BLOCK
 #define RSA_F64_BLOCK 256
 #endif
+#ifndef RSA_F64_ASMEM
+#define RSA_F64_ASMEM 1
+#endif
 #ifndef RSA_F64_MINB32
 #define RSA_F64_MINB32 4
 #endif
@@ -39,9 +42,10 @@ struct F64Cfg {
     // no_instruction).  S = 32 (ND = 20): ~80 registers of state, small code,
     // several independent CTAs per SM.
     static constexpr int BLOCK = (S >= 64) ? RSA_F64_BLOCK : 128;
-    static constexpr int MINB = (S >= 64) ? 256 / RSA_F64_BLOCK : RSA_F64_MINB32;
-    static constexpr bool LOCKSTEP = (S >= 64) && (RSA_F64_BLOCK == 256);
+    static constexpr int MINB = (S >= 64) ? (RSA_F64_BLOCK >= 256 ? 1 : 256 / RSA_F64_BLOCK) : RSA_F64_MINB32;
+    static constexpr bool LOCKSTEP = (S >= 64) && (RSA_F64_BLOCK >= 256);
     static constexpr bool SQR = RSA_F64_SQR;     // dedicated squaring (montsqr) vs montmul(a, a)
+    static constexpr bool ASMEM = (S >= 64) && RSA_F64_ASMEM && SQR;   // montmul's A in the slot's upper half
 };
 
 template <int S>
@@ -105,12 +109,13 @@ modexp_f64_kernel(const __grid_constant__ ModexpF64Params<S> p) {
                 // keeps the kernel's code (and its register allocation) single
                 if (op.kind == RSA_OP_SQR) {
                     if constexpr (F64Cfg<S>::SQR) {
-                        // T_high of the square goes to this thread's slot
+                        // the square's 2 ND digits go to this thread's slot
                         f64::montsqr<ND>(a, nds, p.np52, p.c104, t, reinterpret_cast<uint64_t*>(bsm), stride);
                         continue;
-                    }
+                    } else {
 #pragma unroll
-                    for (int k = 0; k < ND; k++) bsm[k * stride] = a[k];
+                        for (int k = 0; k < ND; k++) bsm[k * stride] = a[k];
+                    }
                 } else if (op.kind == RSA_OP_MUL) {
 #pragma unroll
                     for (int g = 0; g < NP; g++) {
@@ -130,7 +135,8 @@ modexp_f64_kernel(const __grid_constant__ ModexpF64Params<S> p) {
 #pragma unroll
                     for (int k = 0; k < ND; k++) bsm[k * stride] = (k == 0) ? 1.0 : 0.0;
                 }
-                f64::montmul<ND>(a, from_smem, nds, p.np52, p.c104, t);
+                // b occupies digits [0, ND) of the slot; A is parked in [ND, 2 ND)
+                f64::montmul<ND, F64Cfg<S>::ASMEM>(a, from_smem, nds, p.np52, p.c104, t, bsm + ND * stride, stride);
             }
             if (op.flags & RSA_F_STORE) {
 #pragma unroll

@@ -136,9 +136,32 @@ __host__ __device__ __forceinline__ void digits_to_limbs(const uint64_t (&d)[ND]
 // slot to n's digits (with the immediate 2^104 ptxas hoists all ND digits of
 // n into registers instead, and the product schedule starves).  The result digits are returned
 // normalised both as doubles (a) and as integers (ai, for the final store).
-template <int ND, typename BF>
+// volatile load of a thread-private shared-memory digit (not hoisted)
+__host__ __device__ __forceinline__ double ld_digit(const double* p) {
+#ifdef __CUDA_ARCH__
+    double x;
+    asm volatile("ld.volatile.shared.f64 %0, [%1];" : "=d"(x) : "r"((unsigned)__cvta_generic_to_shared(p)));
+    return x;
+#else
+    return *p;
+#endif
+}
+
+// ASMEM: A is parked in this thread's shared-memory slot (aslot[k * stride])
+// for the loop and re-read digit by digit, so its ND registers are free for
+// the product schedule; the result comes back in registers.
+template <int ND, bool ASMEM = false, typename BF>
 __host__ __device__ __forceinline__ void montmul(double (&a)[ND], BF b, const double* __restrict__ nd, uint64_t np,
-                                                 double c104, uint64_t (&t)[ND]) {
+                                                 double c104, uint64_t (&t)[ND], double* aslot = nullptr,
+                                                 int stride = 0) {
+    if constexpr (ASMEM) {
+#pragma unroll
+        for (int k = 0; k < ND; k++) aslot[k * stride] = a[k];
+    }
+    auto A = [&](int k) -> double {
+        if constexpr (ASMEM) return ld_digit(aslot + k * stride);
+        else return a[k];
+    };
 #pragma unroll
     for (int k = 0; k < ND; k++) t[k] = 0;
     uint64_t bias0 = 2 * BL;
@@ -148,8 +171,9 @@ __host__ __device__ __forceinline__ void montmul(double (&a)[ND], BF b, const do
     double bi = b(0);
     uint64_t hp0, c0;
     {
-        const double h0 = fma_rz(a[0], bi, C104);
-        const double l0 = fma_rz(a[0], bi, sub_rn(C2, h0));
+        const double a0 = A(0);
+        const double h0 = fma_rz(a0, bi, C104);
+        const double l0 = fma_rz(a0, bi, sub_rn(C2, h0));
         hp0 = bits(h0);
         c0 = bits(l0);                                   // t[0] = 0
     }
@@ -164,21 +188,24 @@ __host__ __device__ __forceinline__ void montmul(double (&a)[ND], BF b, const do
         const double hq0 = fma_rz(qd, n0, c104);
         const double lq0 = fma_rz(qd, n0, sub_rn(C2, hq0));
         const uint64_t carry = (c0 + bits(lq0) - bias0) >> D;     // column 0 is 0 mod 2^52
-        const double h1 = fma_rz(a[1], bi, C104);
-        const double l1 = fma_rz(a[1], bi, sub_rn(C2, h1));
+        const double a1 = A(1);
+        const double h1 = fma_rz(a1, bi, C104);
+        const double l1 = fma_rz(a1, bi, sub_rn(C2, h1));
         const double hq1 = fma_rz(qd, n1, c104);
         const double lq1 = fma_rz(qd, n1, sub_rn(C2, hq1));
         t[0] = t[1] + bits(l1) + hp0 + bits(lq1) + bits(hq0) + carry;
         // next iteration's column 0: + a_0 b_{i+1}
-        const double hn = fma_rz(a[0], bn, C104);
-        const double ln = fma_rz(a[0], bn, sub_rn(C2, hn));
+        const double a0 = A(0);
+        const double hn = fma_rz(a0, bn, C104);
+        const double ln = fma_rz(a0, bn, sub_rn(C2, hn));
         const uint64_t c0n = t[0] + bits(ln);
         const double qnext = digit_to_double(((c0n & M52) * np) & M52);
         uint64_t hp = bits(h1), hqp = bits(hq1);
 #pragma unroll
         for (int j = 2; j < ND; j++) {
-            const double h = fma_rz(a[j], bi, C104);
-            const double l = fma_rz(a[j], bi, sub_rn(C2, h));
+            const double aj = A(j);
+            const double h = fma_rz(aj, bi, C104);
+            const double l = fma_rz(aj, bi, sub_rn(C2, h));
             t[j - 1] = t[j] + bits(l) + hp;
             hp = bits(h);
         }

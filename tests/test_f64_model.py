@@ -59,11 +59,12 @@ def test_montmul_f64_matches_definition(model, S):
             a, b = 0, rng.randrange(2 * n)
         else:
             a, b = rng.randrange(2 * n), rng.randrange(2 * n)
-        out = model(f"M {S} {n:x} {a:x} {b:x}")
-        assert out != "MISMATCH", "double digits disagree with integer digits"
-        r = int(out, 16)
-        assert r < 2 * n, "almost-Montgomery bound r < 2n"
-        assert r % n == a * b * rinv % n
+        for op in "MA":                            # registers / A parked in shared memory
+            out = model(f"{op} {S} {n:x} {a:x} {b:x}")
+            assert out != "MISMATCH", "double digits disagree with integer digits"
+            r = int(out, 16)
+            assert r < 2 * n, "almost-Montgomery bound r < 2n"
+            assert r % n == a * b * rinv % n
 
 
 @pytest.mark.parametrize("S", [16, 64])

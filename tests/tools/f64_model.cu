@@ -60,7 +60,7 @@ static void run(char op, char** tok) {
     for (int it = 0; it < 7; it++) inv *= 2 - nu[0] * inv;
     const uint64_t np = (0 - inv) & M52;
     uint64_t r[ND];
-    if (op == 'M' || op == 'S') {
+    if (op == 'M' || op == 'S' || op == 'A') {
         // a, b may be up to 2n: given as digits-of-hex over ND*52 bits
         constexpr int SW = (52 * ND + 31) / 32;
         auto av = parse_hex(tok[1], SW), bv = parse_hex(tok[2], SW);
@@ -81,7 +81,12 @@ static void run(char op, char** tok) {
             uint64_t th[2 * ND];
             montsqr<ND>(ad, nd, np, C104, r, th, 1);
         } else {
-            montmul<ND>(ad, [&](int i) { return bd[i]; }, nd, np, C104, r);
+            if (op == 'A') {              // the ASMEM variant (A parked in a strided slot)
+                double slot[3 * ND];
+                montmul<ND, true>(ad, [&](int i) { return bd[i]; }, nd, np, C104, r, slot + 1, 3);
+            } else {
+                montmul<ND>(ad, [&](int i) { return bd[i]; }, nd, np, C104, r);
+            }
         }
         for (int k = 0; k < ND; k++)
             if ((uint64_t)ad[k] != r[k]) { printf("MISMATCH\n"); return; }
