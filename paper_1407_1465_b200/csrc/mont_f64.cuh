@@ -42,9 +42,20 @@
 #include <cstring>
 #endif
 
+#ifndef RSA_F64_MU
+#define RSA_F64_MU 1      // CIOS loop trips unrolled (A/B knob)
+#endif
+#ifndef RSA_F64_RU
+#define RSA_F64_RU 4      // squaring's reduction loop trips unrolled at ND >= 40 (A/B knob:
+#endif                    // 1/2/4/5 -> 565K/581K/590K/585K RSA-2048 decrypts/s)
+#ifndef RSA_F64_RU_SMALL
+#define RSA_F64_RU_SMALL 1   // ... at ND < 40
+#endif
+
 namespace rsa_b200 {
 namespace f64 {
 
+constexpr int kMU = RSA_F64_MU, kRU = RSA_F64_RU, kRUs = RSA_F64_RU_SMALL;
 constexpr int D = 52;
 constexpr uint64_t M52 = (1ull << 52) - 1;
 constexpr uint64_t BL = 0x433ull << 52;            // bit pattern of 2^52
@@ -179,7 +190,7 @@ __host__ __device__ __forceinline__ void montmul(double (&a)[ND], BF b, const do
     }
     double qd = digit_to_double(((c0 & M52) * np) & M52);
 #ifdef __CUDA_ARCH__
-#pragma unroll 1
+#pragma unroll kMU
 #endif
     for (int i = 0; i < ND; i++) {
         const double bn = b(i + 1 < ND ? i + 1 : i);
@@ -250,7 +261,7 @@ __host__ __device__ __forceinline__ void montmul(double (&a)[ND], BF b, const do
 //   2. Reduction-only CIOS on t: q = t_0 n' mod 2^52; t = (t + q n) / 2^52,
 //      ND times (loop, not unrolled).
 //   3. t + T_high, normalised: T / R + Q n / R < 4n^2/R + n < 2n.
-template <int ND>
+template <int ND, int RU = (ND >= 40 ? kRU : kRUs)>
 __host__ __device__ __forceinline__ void montsqr(double (&a)[ND], const double* __restrict__ nd, uint64_t np,
                                                  double c104, uint64_t (&t)[ND], uint64_t* th, int stride) {
     // 1. T = A^2
@@ -298,7 +309,7 @@ __host__ __device__ __forceinline__ void montsqr(double (&a)[ND], const double* 
     uint64_t bias0 = BL;
     double qd = digit_to_double(((t[0] & M52) * np) & M52);
 #ifdef __CUDA_ARCH__
-#pragma unroll 1
+#pragma unroll RU
 #endif
     for (int i = 0; i < ND; i++) {
         double n0, n1;
