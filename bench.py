@@ -317,7 +317,8 @@ def run_ours(args, rank, world, local_rank):
         hp = R.rsa_plan_info(key["d"] % (p_ - 1), p_, hb)
         hq = R.rsa_plan_info(key["d"] % (q_ - 1), q_, hb)
         plans = [dict(hp, montmuls=hp["montmuls"] + hq["montmuls"], squarings=hp["squarings"] + hq["squarings"],
-                      products=hp["products"] + hq["products"], window=hp["window"], exp_bits=hp["exp_bits"])]
+                      products=hp["products"] + hq["products"], window=hp["window"], exp_bits=hp["exp_bits"],
+                      digit_products=hp["digit_products"] + hq["digit_products"])]
     else:
         exps = [0]
         plans = [R.rsa_multi_plan_info(nb, 0, mr=True)]
@@ -419,12 +420,13 @@ def run_ours(args, rank, world, local_rank):
     products = count * plans[dom]["products"]
     achieved = products / (leg_ms[dom] / 1e3) / 1e12
     peak = R_PRODUCTS_PER_CLK_PER_SM * sms * f_max * 1e6 / 1e12
-    fp64 = kind == "batch" and plans[dom].get("fp64_digits", 0) > 0
+    fp64 = kind in ("batch", "crt") and plans[dom].get("fp64_digits", 0) > 0
     roofline = {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "Tprod/s", "frac": achieved / peak,
                 "traffic": ncu_traffic(key_name, legs[dom][0], count),
                 "traffic_unit": "bytes per launch", "algorithmic_bytes": count * s * 4 * 2,
                 "kernel": ({"multi": f"modexp_multi_kernel<{S}>", "mr": f"modexp_multi_kernel<{S}> (MR mode)",
-                            "crt": f"2 x modexp_kernel<{S}> + crt_split/combine (half-width CRT legs; products of both)"}.get(
+                            "crt": f"2 x {batch_kernel_name(S, fp64)} + crt_split/combine (half-width CRT legs; "
+                                   f"products of both)"}.get(
                     kind, batch_kernel_name(S, fp64))) + f" ({legs[dom][0]})",
                 "algorithmic": f"{plans[dom]['products']} 32x32->64 limb products/packet "
                                f"({plans[dom]['squarings']} squarings x "
