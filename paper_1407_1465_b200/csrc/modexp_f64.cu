@@ -30,6 +30,9 @@ namespace rsa_b200 {
 #ifndef RSA_F64_ASMEM
 #define RSA_F64_ASMEM 1
 #endif
+#ifndef RSA_F64_MINB128
+#define RSA_F64_MINB128 2
+#endif
 #ifndef RSA_F64_MINB32
 #define RSA_F64_MINB32 4
 #endif
@@ -41,11 +44,17 @@ struct F64Cfg {
     // of SASS, and drifting warps stall on instruction fetch (ncu:
     // no_instruction).  S = 32 (ND = 20): ~80 registers of state, small code,
     // several independent CTAs per SM.
-    static constexpr int BLOCK = (S >= 64) ? RSA_F64_BLOCK : 128;
-    static constexpr int MINB = (S >= 64) ? (RSA_F64_BLOCK >= 256 ? 1 : 256 / RSA_F64_BLOCK) : RSA_F64_MINB32;
-    static constexpr bool LOCKSTEP = (S >= 64) && (RSA_F64_BLOCK >= 256);
-    static constexpr bool SQR = RSA_F64_SQR;     // dedicated squaring (montsqr) vs montmul(a, a)
-    static constexpr bool ASMEM = (S >= 64) && RSA_F64_ASMEM && SQR;   // montmul's A in the slot's upper half
+    static constexpr int BLOCK = (S == 64) ? RSA_F64_BLOCK : 128;
+    static constexpr int MINB = (S == 64) ? (RSA_F64_BLOCK >= 256 ? 1 : 256 / RSA_F64_BLOCK)
+                                          : (S == 32 ? RSA_F64_MINB32 : RSA_F64_MINB128);
+    static constexpr bool LOCKSTEP = (S == 64) && (RSA_F64_BLOCK >= 256);
+    // S = 128 (ND = 80): the square's 2 ND digits and A + B slots do not fit shared memory at
+    // 8 warps/SM, so every op is the CIOS multiply with A parked in a single ND-digit slot and B
+    // read in place (the slot itself for squarings, the window table in global memory, or a
+    // per-block constant): ND^2 products more per squaring, no squaring code.
+    static constexpr bool ONESLOT = (S >= 128);
+    static constexpr bool SQR = RSA_F64_SQR && !ONESLOT;   // dedicated squaring (montsqr) vs montmul(a, a)
+    static constexpr bool ASMEM = ONESLOT || ((S >= 64) && RSA_F64_ASMEM && SQR);   // montmul's A parked in smem
 };
 
 template <int S>
@@ -64,7 +73,14 @@ modexp_f64_kernel(const __grid_constant__ ModexpF64Params<S> p) {
     // n's digits, one shared copy per block (read by the volatile pair loads
     // of mont_f64.cuh)
     __shared__ __align__(16) double nds[ND];
-    for (int k = threadIdx.x; k < ND; k += blockDim.x) nds[k] = p.nd[k];
+    __shared__ __align__(16) double cst[F64Cfg<S>::ONESLOT ? 2 * ND : 1];   // R^2 mod n, 1 (ONESLOT)
+    for (int k = threadIdx.x; k < ND; k += blockDim.x) {
+        nds[k] = p.nd[k];
+        if constexpr (F64Cfg<S>::ONESLOT) {
+            cst[k] = p.r2d[k];
+            cst[ND + k] = (k == 0) ? 1.0 : 0.0;
+        }
+    }
     __syncthreads();
 
     // every thread runs the same number of trips (uniform barriers); an
@@ -91,7 +107,15 @@ modexp_f64_kernel(const __grid_constant__ ModexpF64Params<S> p) {
         };
         double a[ND];
         uint64_t t[ND];
-        load_input(a);
+        if constexpr (F64Cfg<S>::ONESLOT) {
+            // A lives in this thread's slot
+            double x[ND];
+            load_input(x);
+#pragma unroll
+            for (int k = 0; k < ND; k++) bsm[k * stride] = x[k];
+        } else {
+            load_input(a);
+        }
         auto from_smem = [&](int i) { return bsm[i * stride]; };
 
         for (int i = 0; i < ip.nops; i++) {
@@ -100,9 +124,31 @@ modexp_f64_kernel(const __grid_constant__ ModexpF64Params<S> p) {
 #pragma unroll
                 for (int g = 0; g < NP; g++) {
                     const double2 v = table[((size_t)op.lidx * NP + g) * nthr + gtid];
-                    a[2 * g] = v.x; a[2 * g + 1] = v.y;
+                    if constexpr (F64Cfg<S>::ONESLOT) {
+                        bsm[(2 * g) * stride] = v.x;
+                        bsm[(2 * g + 1) * stride] = v.y;
+                    } else {
+                        a[2 * g] = v.x; a[2 * g + 1] = v.y;
+                    }
                 }
             }
+            if constexpr (F64Cfg<S>::ONESLOT) {
+                // b(i) = bp[i * bs]: generic loads from the A slot (squaring), this
+                // thread's table entry (global), or the per-block constants
+                // digit i at bp[(i >> 1) * P + (i & 1) * Q]: one formula for the
+                // digit-major slot, the pair-interleaved table and the constants
+                const double* bp;
+                size_t P, Q;
+                if (op.kind == RSA_OP_SQR) { bp = bsm; P = 2 * (size_t)stride; Q = stride; }
+                else if (op.kind == RSA_OP_MUL) {
+                    bp = reinterpret_cast<const double*>(table) + (size_t)op.bidx * ND * nthr + 2 * (size_t)gtid;
+                    P = 2 * (size_t)nthr; Q = 1;
+                } else if (op.kind == RSA_OP_R2) { bp = cst; P = 2; Q = 1; }
+                else { bp = cst + ND; P = 2; Q = 1; }   // RSA_OP_ONE (plans for this class carry no MULX)
+                auto bget = [&](int i) -> double { return bp[(size_t)(i >> 1) * P + (i & 1) * Q]; };
+                for (int r = 0; r < op.rep; r++)
+                    f64::montmul<ND, true, decltype(bget), true>(a, bget, nds, p.np52, p.c104, t, bsm, stride);
+            } else
             for (int r = 0; r < op.rep; r++) {
                 if constexpr (F64Cfg<S>::LOCKSTEP) __syncthreads();
                 // stage the b operand in this thread's slot; one montmul call site
@@ -140,8 +186,13 @@ modexp_f64_kernel(const __grid_constant__ ModexpF64Params<S> p) {
             }
             if (op.flags & RSA_F_STORE) {
 #pragma unroll
-                for (int g = 0; g < NP; g++)
-                    table[((size_t)op.sidx * NP + g) * nthr + gtid] = make_double2(a[2 * g], a[2 * g + 1]);
+                for (int g = 0; g < NP; g++) {
+                    if constexpr (F64Cfg<S>::ONESLOT)
+                        table[((size_t)op.sidx * NP + g) * nthr + gtid] =
+                            make_double2(bsm[(2 * g) * stride], bsm[(2 * g + 1) * stride]);
+                    else
+                        table[((size_t)op.sidx * NP + g) * nthr + gtid] = make_double2(a[2 * g], a[2 * g + 1]);
+                }
             }
         }
 
@@ -167,7 +218,7 @@ template <int S>
 static cudaError_t launch_f64(const void* params, int sms, cudaStream_t stream, int* grid_out, int* block_out,
                               size_t* slots_out, bool query_only) {
     const int block = F64Cfg<S>::BLOCK;
-    const size_t smem = sizeof(double) * F64Cfg<S>::ND * (F64Cfg<S>::SQR ? 2 : 1) * block;
+    const size_t smem = sizeof(double) * F64Cfg<S>::ND * ((F64Cfg<S>::SQR || F64Cfg<S>::ASMEM) && !F64Cfg<S>::ONESLOT ? 2 : 1) * block;
     static int occ = -1;
     if (occ < 0) {
         cudaError_t e = cudaFuncSetAttribute(modexp_f64_kernel<S>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -198,6 +249,7 @@ cudaError_t rsa_b200_launch_f64(int S, const void* params, int sms, cudaStream_t
     switch (S) {
     case 32: return launch_f64<32>(params, sms, stream, grid, block, slots, query_only);
     case 64: return launch_f64<64>(params, sms, stream, grid, block, slots, query_only);
+    case 128: return launch_f64<128>(params, sms, stream, grid, block, slots, query_only);
     default: return cudaErrorInvalidValue;
     }
 }

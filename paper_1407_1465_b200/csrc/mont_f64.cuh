@@ -66,7 +66,8 @@ constexpr double C2 = 20282409603651674927546878656512.0;     // 2^104 + 2^52
 constexpr double C52 = 4503599627370496.0;                      // 2^52
 
 // digits needed for a Montgomery radix R = 2^(52 ND) > 4n with n < 2^(32 S)
-template <int S> struct Digits { static constexpr int ND = (32 * S + 2 + D - 1) / D; };
+// (rounded up to even: the kernels move digit pairs; plan.h rsa_f64_digits is the same)
+template <int S> struct Digits { static constexpr int ND = ((32 * S + 2 + D - 1) / D + 1) / 2 * 2; };
 
 __host__ __device__ __forceinline__ uint64_t bits(double x) {
 #ifdef __CUDA_ARCH__
@@ -161,11 +162,14 @@ __host__ __device__ __forceinline__ double ld_digit(const double* p) {
 // ASMEM: A is parked in this thread's shared-memory slot (aslot[k * stride])
 // for the loop and re-read digit by digit, so its ND registers are free for
 // the product schedule; the result comes back in registers.
-template <int ND, bool ASMEM = false, typename BF>
+// AIN: A lives in the slot (no copy in, the result digits go back to the slot
+// and a[] is not touched).
+template <int ND, bool ASMEM = false, typename BF, bool AIN = false>
 __host__ __device__ __forceinline__ void montmul(double (&a)[ND], BF b, const double* __restrict__ nd, uint64_t np,
                                                  double c104, uint64_t (&t)[ND], double* aslot = nullptr,
                                                  int stride = 0) {
-    if constexpr (ASMEM) {
+    static_assert(!AIN || ASMEM, "AIN needs the slot");
+    if constexpr (ASMEM && !AIN) {
 #pragma unroll
         for (int k = 0; k < ND; k++) aslot[k * stride] = a[k];
     }
@@ -244,7 +248,8 @@ __host__ __device__ __forceinline__ void montmul(double (&a)[ND], BF b, const do
         const uint64_t v = t[p] - (2 * BH + (uint64_t)(ND - 1 - p) * BETA) + carry;
         t[p] = v & M52;
         carry = v >> D;
-        a[p] = digit_to_double(t[p]);
+        if constexpr (AIN) aslot[p * stride] = digit_to_double(t[p]);
+        else a[p] = digit_to_double(t[p]);
     }
 }
 

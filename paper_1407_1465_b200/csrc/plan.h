@@ -68,7 +68,8 @@ struct ModexpParams {
 // FP64-pipe kernel (mont_f64.cuh) for class S: digits of 52 bits, R = 2^(52 ND)
 // with 4n < R.  The integer params come first, so the blob also serves the
 // IMAD kernel of the same class (patch_params casts it to ModexpParams<S>).
-constexpr int rsa_f64_digits(int S) { return (32 * S + 2 + 51) / 52; }
+// (rounded up to an even count: table entries move as digit pairs)
+constexpr int rsa_f64_digits(int S) { return ((32 * S + 2 + 51) / 52 + 1) / 2 * 2; }
 
 template <int S>
 struct ModexpF64Params {

@@ -103,7 +103,7 @@ static int width_class(int s_io) {
 
 // Build the op list for window width w; returns false if it does not fit.
 static bool build_ops(const BN& e, int w, int cap, std::vector<RsaOp>* ops, int* ntab, long long* mm,
-                      long long* sq) {
+                      long long* sq, bool allow_mulx = true) {
     std::vector<Window> win = recode(e, w);
     const int nodd = 1 << (w - 1);
     const int g2 = nodd;                      // table index of g^2 (w > 1)
@@ -153,8 +153,8 @@ static bool build_ops(const BN& e, int w, int cap, std::vector<RsaOp>* ops, int*
     // the scan ends with a multiply by g itself (last digit 1, e.g. every odd
     // public exponent at w = 1), that multiply takes the raw input x instead of
     // g R, which lands outside Montgomery form directly: one montmul fewer.
-    if (!pending_load && ops->back().kind == RSA_OP_MUL && ops->back().bidx == 0 && ops->back().flags == 0 &&
-        ops->back().rep == 1) {
+    if (allow_mulx && !pending_load && ops->back().kind == RSA_OP_MUL && ops->back().bidx == 0 &&
+        ops->back().flags == 0 && ops->back().rep == 1) {
         ops->back().kind = RSA_OP_MULX;
     } else {
         push(RSA_OP_ONE, 1, pending_load ? RSA_F_LOADA : 0, 0, first, 0);
@@ -189,7 +189,7 @@ static void fill_f64(ModexpF64Params<S>* f, const BN& n) {
 
 template <int S>
 static void fill_params(Plan& pl, const BN& n, const std::vector<RsaOp>& ops) {
-    if constexpr (S == 64 || S == 32) {
+    if constexpr (S == 64 || S == 32 || S == 128) {
         pl.params.assign(sizeof(ModexpF64Params<S>), 0);
         fill_f64<S>(reinterpret_cast<ModexpF64Params<S>*>(pl.params.data()), n);
     } else {
@@ -272,7 +272,9 @@ static int get_plan_ptr(const uint32_t* exp, const uint32_t* n, int nbits, std::
             std::vector<RsaOp> ops;
             int ntab;
             long long mm, sq;
-            if (!build_ops(E, w, rsa_ops_cap(pl.S), &ops, &ntab, &mm, &sq)) continue;
+            // the 4096-bit FP64 kernel has one shared-memory slot (A): no raw-input multiply
+            const bool mulx = !(pl.S == 128 && rsa_b200_is_f64(128));
+            if (!build_ops(E, w, rsa_ops_cap(pl.S), &ops, &ntab, &mm, &sq, mulx)) continue;
             // minimise executed limb products (squarings are cheaper when the
             // class has the dedicated squaring kernel)
             const long long S = pl.S;
@@ -642,7 +644,8 @@ int rsa_plan_info(const uint32_t* exp, const uint32_t* n, int nbits, rsa_plan_in
     if (rsa_b200_is_f64(pl.S)) {
         const long long nd = rsa_f64_digits(pl.S);
         info->fp64_digits = (int)nd;
-        info->digit_products = pl.squarings * (nd * (nd + 1) / 2 + nd * nd) + (pl.montmuls - pl.squarings) * 2 * nd * nd;
+        const long long sqd = (pl.S < 128) ? nd * (nd + 1) / 2 + nd * nd : 2 * nd * nd;   // S = 128: no montsqr
+        info->digit_products = pl.squarings * sqd + (pl.montmuls - pl.squarings) * 2 * nd * nd;
     }
     const int sms = device_sms();
     if (sms) {
