@@ -739,10 +739,10 @@ static bool rsa_b200_f64(int S) {
         const char* e = getenv("RSA_B200_F64");
         v = (e && e[0] == '0') ? 0 : 1;
     }
-    static int v4 = -1;     // 4096-bit class: opt-in (RSA_B200_F64_4096=1) until measured faster
+    static int v4 = -1;     // 4096-bit class: RSA_B200_F64_4096=0 selects the integer lane-pair kernel
     if (v4 < 0) {
         const char* e = getenv("RSA_B200_F64_4096");
-        v4 = (e && e[0] == '1') ? 1 : 0;
+        v4 = (e && e[0] == '0') ? 0 : 1;
     }
     return v == 1 && ((S == 64 && !rsa_b200_shape64()) || S == 32 || (S == 128 && v4 == 1));
 }

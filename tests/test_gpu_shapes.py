@@ -1,6 +1,7 @@
 """The alternative kernel shapes kept for measurement ('chosen by
-measurement'): the 2048-bit class on the integer pipe or the FP64 pipe
-(RSA_B200_F64=0/1), 2048-bit as a 2-lane group (RSA_B200_SHAPE64=group2) and
+measurement'): the 1024/2048-bit classes on the integer pipe or the FP64 pipe
+(RSA_B200_F64=0/1), the 4096-bit integer lane-pair kernel (RSA_B200_F64_4096=0),
+2048-bit as a 2-lane group (RSA_B200_SHAPE64=group2) and
 4096-bit as a 4-lane group (RSA_B200_TPI128=4), and the thread-per-packet
 kernel for the small widths (RSA_B200_SMALL=0, instead of the multi-packet
 one) stay bit-exact vs the oracle.
@@ -37,8 +38,10 @@ print("shape ok")
                                            ("RSA_B200_F64=1", "rsa1536", 300),
                                            ("RSA_B200_SHAPE64=group2", "rsa2048", 300),
                                            ("RSA_B200_SHAPE64=group2", "rsa1536", 300),
-                                           ("RSA_B200_TPI128=4", "rsa4096", 60),
-                                           ("RSA_B200_TPI128=4", "rsa3072", 60),
+                                           ("RSA_B200_F64_4096=0", "rsa4096", 60),
+                                           ("RSA_B200_F64_4096=0", "rsa3072", 60),
+                                           ("RSA_B200_F64_4096=0,RSA_B200_TPI128=4", "rsa4096", 60),
+                                           ("RSA_B200_F64_4096=0,RSA_B200_TPI128=4", "rsa3072", 60),
                                            ("RSA_B200_SMALL=0", "rsa64", 3001),
                                            ("RSA_B200_SMALL=0", "rsa128", 3001),
                                            ("RSA_B200_SMALL=0", "toy17947", 3001)])
@@ -46,7 +49,7 @@ def test_alternative_shapes(env, key, count):
     torch = pytest.importorskip("torch")
     if not torch.cuda.is_available():
         pytest.skip("no CUDA device")
-    k, v = env.split("=")
+    kv = dict(x.split("=") for x in env.split(","))
     r = subprocess.run([sys.executable, "-c", SCRIPT, key, str(count)], capture_output=True, text=True,
-                       timeout=900, env=dict(os.environ, **{k: v}))
+                       timeout=900, env=dict(os.environ, **kv))
     assert r.returncode == 0 and "shape ok" in r.stdout, (r.stdout + r.stderr)[-2000:]
