@@ -47,7 +47,10 @@ struct F64Cfg {
     static constexpr int BLOCK = (S == 64) ? RSA_F64_BLOCK : 128;
     static constexpr int MINB = (S == 64) ? (RSA_F64_BLOCK >= 256 ? 1 : 256 / RSA_F64_BLOCK)
                                           : (S == 32 ? RSA_F64_MINB32 : RSA_F64_MINB128);
-    static constexpr bool LOCKSTEP = (S == 64) && (RSA_F64_BLOCK >= 256);
+#ifndef RSA_F64_LOCK
+#define RSA_F64_LOCK 0      // A/B: lockstep barriers with 2 x 128-thread CTAs (557K vs 589K)
+#endif
+    static constexpr bool LOCKSTEP = (S == 64) && (RSA_F64_BLOCK >= 256 || RSA_F64_LOCK);
     // S = 128 (ND = 80): the square's 2 ND digits and A + B slots do not fit shared memory at
     // 8 warps/SM, so every op is the CIOS multiply with A parked in a single ND-digit slot and B
     // read in place (the slot itself for squarings, the window table in global memory, or a
