@@ -30,6 +30,12 @@ namespace rsa_b200 {
 #ifndef RSA_F64_ASMEM
 #define RSA_F64_ASMEM 1
 #endif
+#ifndef RSA_F64_FUSEJ
+#define RSA_F64_FUSEJ 0     // 4096-bit kernel: one fused j-loop (A/B: 54.4K vs 56.4K, no spills but less overlap)
+#endif
+#ifndef RSA_F64_FUSEJ64
+#define RSA_F64_FUSEJ64 0   // 1024/2048-bit multiply: fused j-loop (A/B)
+#endif
 #ifndef RSA_F64_MINB128
 #define RSA_F64_MINB128 2
 #endif
@@ -150,7 +156,8 @@ modexp_f64_kernel(const __grid_constant__ ModexpF64Params<S> p) {
                 else { bp = cst + ND; P = 2; Q = 1; }   // RSA_OP_ONE (plans for this class carry no MULX)
                 auto bget = [&](int i) -> double { return bp[(size_t)(i >> 1) * P + (i & 1) * Q]; };
                 for (int r = 0; r < op.rep; r++)
-                    f64::montmul<ND, true, decltype(bget), true>(a, bget, nds, p.np52, p.c104, t, bsm, stride);
+                    f64::montmul<ND, true, decltype(bget), true, RSA_F64_FUSEJ>(a, bget, nds, p.np52, p.c104, t, bsm,
+                                                                              stride);
             } else
             for (int r = 0; r < op.rep; r++) {
                 if constexpr (F64Cfg<S>::LOCKSTEP) __syncthreads();
@@ -185,7 +192,8 @@ modexp_f64_kernel(const __grid_constant__ ModexpF64Params<S> p) {
                     for (int k = 0; k < ND; k++) bsm[k * stride] = (k == 0) ? 1.0 : 0.0;
                 }
                 // b occupies digits [0, ND) of the slot; A is parked in [ND, 2 ND)
-                f64::montmul<ND, F64Cfg<S>::ASMEM>(a, from_smem, nds, p.np52, p.c104, t, bsm + ND * stride, stride);
+                f64::montmul<ND, F64Cfg<S>::ASMEM, decltype(from_smem), false, RSA_F64_FUSEJ64 != 0>(
+                    a, from_smem, nds, p.np52, p.c104, t, bsm + ND * stride, stride);
             }
             if (op.flags & RSA_F_STORE) {
 #pragma unroll

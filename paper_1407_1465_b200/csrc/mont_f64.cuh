@@ -164,7 +164,9 @@ __host__ __device__ __forceinline__ double ld_digit(const double* p) {
 // the product schedule; the result comes back in registers.
 // AIN: A lives in the slot (no copy in, the result digits go back to the slot
 // and a[] is not touched).
-template <int ND, bool ASMEM = false, typename BF, bool AIN = false>
+// FUSEJ: one j-loop for both product rows (A b_i and q n), each column written
+// once per iteration (fewer live partial results; for the 4096-bit kernel).
+template <int ND, bool ASMEM = false, typename BF, bool AIN = false, bool FUSEJ = false>
 __host__ __device__ __forceinline__ void montmul(double (&a)[ND], BF b, const double* __restrict__ nd, uint64_t np,
                                                  double c104, uint64_t (&t)[ND], double* aslot = nullptr,
                                                  int stride = 0) {
@@ -216,6 +218,21 @@ __host__ __device__ __forceinline__ void montmul(double (&a)[ND], BF b, const do
         const uint64_t c0n = t[0] + bits(ln);
         const double qnext = digit_to_double(((c0n & M52) * np) & M52);
         uint64_t hp = bits(h1), hqp = bits(hq1);
+        if constexpr (FUSEJ) {
+#pragma unroll
+            for (int j = 2; j < ND; j++) {
+                const double aj = A(j);
+                const double h = fma_rz(aj, bi, C104);
+                const double l = fma_rz(aj, bi, sub_rn(C2, h));
+                double nj = n1;
+                if ((j & 1) == 0) nd_pair(nd, j / 2, nj, n1);
+                const double hq = fma_rz(qd, nj, c104);
+                const double lq = fma_rz(qd, nj, sub_rn(C2, hq));
+                t[j - 1] = t[j] + bits(l) + hp + bits(lq) + hqp;
+                hp = bits(h);
+                hqp = bits(hq);
+            }
+        } else {
 #pragma unroll
         for (int j = 2; j < ND; j++) {
             const double aj = A(j);
@@ -232,6 +249,7 @@ __host__ __device__ __forceinline__ void montmul(double (&a)[ND], BF b, const do
             const double l = fma_rz(qd, nj, sub_rn(C2, h));
             t[j - 1] += bits(l) + hqp;
             hqp = bits(h);
+        }
         }
         t[ND - 1] = hp + hqp;
         c0 = c0n;

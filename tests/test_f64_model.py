@@ -59,7 +59,7 @@ def test_montmul_f64_matches_definition(model, S):
             a, b = 0, rng.randrange(2 * n)
         else:
             a, b = rng.randrange(2 * n), rng.randrange(2 * n)
-        for op in "MAI":                           # registers / A parked / A living in the slot
+        for op in "MAIF":                          # registers / A parked / A living in the slot (+ fused rows)
             out = model(f"{op} {S} {n:x} {a:x} {b:x}")
             assert out != "MISMATCH", "double digits disagree with integer digits"
             r = int(out, 16)

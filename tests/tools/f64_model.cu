@@ -60,7 +60,7 @@ static void run(char op, char** tok) {
     for (int it = 0; it < 7; it++) inv *= 2 - nu[0] * inv;
     const uint64_t np = (0 - inv) & M52;
     uint64_t r[ND];
-    if (op == 'M' || op == 'S' || op == 'A' || op == 'I') {
+    if (op == 'M' || op == 'S' || op == 'A' || op == 'I' || op == 'F') {
         // a, b may be up to 2n: given as digits-of-hex over ND*52 bits
         constexpr int SW = (52 * ND + 31) / 32;
         auto av = parse_hex(tok[1], SW), bv = parse_hex(tok[2], SW);
@@ -84,11 +84,12 @@ static void run(char op, char** tok) {
             if (op == 'A') {              // the ASMEM variant (A parked in a strided slot)
                 double slot[3 * ND];
                 montmul<ND, true>(ad, [&](int i) { return bd[i]; }, nd, np, C104, r, slot + 1, 3);
-            } else if (op == 'I') {       // A lives in the slot (the 4096-bit kernel)
+            } else if (op == 'I' || op == 'F') {   // A lives in the slot (the 4096-bit kernel)
                 double slot[3 * ND], dummy[ND];
                 for (int k = 0; k < ND; k++) { slot[1 + 3 * k] = ad[k]; dummy[k] = -1.0; }
                 auto bf = [&](int i) { return bd[i]; };
-                montmul<ND, true, decltype(bf), true>(dummy, bf, nd, np, C104, r, slot + 1, 3);
+                if (op == 'F') montmul<ND, true, decltype(bf), true, true>(dummy, bf, nd, np, C104, r, slot + 1, 3);
+                else montmul<ND, true, decltype(bf), true>(dummy, bf, nd, np, C104, r, slot + 1, 3);
                 for (int k = 0; k < ND; k++) ad[k] = slot[1 + 3 * k];
             } else {
                 montmul<ND>(ad, [&](int i) { return bd[i]; }, nd, np, C104, r);
