@@ -42,6 +42,9 @@
 #include <cstring>
 #endif
 
+#ifndef RSA_F64_LOOKAHEAD
+#define RSA_F64_LOOKAHEAD 0   // carry-lookahead normalisation (A/B)
+#endif
 #ifndef RSA_F64_MU
 #define RSA_F64_MU 1      // CIOS loop trips unrolled (A/B knob)
 #endif
@@ -148,6 +151,42 @@ __host__ __device__ __forceinline__ void digits_to_limbs(const uint64_t (&d)[ND]
 // slot to n's digits (with the immediate 2^104 ptxas hoists all ND digits of
 // n into registers instead, and the product schedule starves).  The result digits are returned
 // normalised both as doubles (a) and as integers (ai, for the final store).
+// t[p] (true column values < 2^62) -> digits < 2^52 of the same number (the
+// carry out of the top column is 0 by the callers' bounds).  Carry-lookahead
+// instead of a 2 ND-deep serial chain: one local pass (low 52 bits + the
+// previous column's high bits leaves a 0/1 carry per column), then the single-bit
+// carries resolve with one 64-bit addition on bitmasks (generate G, propagate
+// P: carry-in = (G + (G | P)) ^ P), then one more local pass.
+template <int ND>
+__host__ __device__ __forceinline__ void normalize(uint64_t (&t)[ND]) {
+    constexpr int NW = (ND + 63) / 64;
+    uint64_t G[NW], P[NW];
+#pragma unroll
+    for (int w = 0; w < NW; w++) { G[w] = 0; P[w] = 0; }
+    uint64_t hprev = 0;
+#pragma unroll
+    for (int p = 0; p < ND; p++) {
+        const uint64_t v = t[p];
+        const uint64_t w = (v & M52) + hprev;
+        hprev = v >> D;
+        const uint64_t r = w & M52;
+        t[p] = r;
+        G[p >> 6] |= (w >> D) << (p & 63);
+        P[p >> 6] |= (uint64_t)(r == M52) << (p & 63);
+    }
+    uint64_t C[NW], cin = 0;
+#pragma unroll
+    for (int w = 0; w < NW; w++) {
+        const uint64_t b = G[w] | P[w];
+        const uint64_t s1 = G[w] + b;
+        const uint64_t s2 = s1 + cin;
+        cin = (s1 < G[w]) | (s2 < s1);
+        C[w] = s2 ^ P[w];
+    }
+#pragma unroll
+    for (int p = 0; p < ND; p++) t[p] = (t[p] + ((C[p >> 6] >> (p & 63)) & 1)) & M52;
+}
+
 // volatile load of a thread-private shared-memory digit (not hoisted)
 __host__ __device__ __forceinline__ double ld_digit(const double* p) {
 #ifdef __CUDA_ARCH__
@@ -260,6 +299,16 @@ __host__ __device__ __forceinline__ void montmul(double (&a)[ND], BF b, const do
     }
     // remove the exponent fields and propagate carries: column p now carries
     // 2 BH + (ND-1-p) BETA (mod 2^64) on top of its true value
+#if RSA_F64_LOOKAHEAD
+#pragma unroll
+    for (int p = 0; p < ND; p++) t[p] -= 2 * BH + (uint64_t)(ND - 1 - p) * BETA;
+    normalize<ND>(t);
+#pragma unroll
+    for (int p = 0; p < ND; p++) {
+        if constexpr (AIN) aslot[p * stride] = digit_to_double(t[p]);
+        else a[p] = digit_to_double(t[p]);
+    }
+#else
     uint64_t carry = 0;
 #pragma unroll
     for (int p = 0; p < ND; p++) {
@@ -269,6 +318,7 @@ __host__ __device__ __forceinline__ void montmul(double (&a)[ND], BF b, const do
         if constexpr (AIN) aslot[p * stride] = digit_to_double(t[p]);
         else a[p] = digit_to_double(t[p]);
     }
+#endif
 }
 
 // A <- A^2 R^-1 (mod n), result < 2n for A < 2n (squarings are ~85% of a
@@ -359,6 +409,13 @@ __host__ __device__ __forceinline__ void montsqr(double (&a)[ND], const double* 
         bias0 += BL + BH;
     }
     // 3. + T_high, normalise (column p carries BH + (ND-1-p)(BL+BH))
+#if RSA_F64_LOOKAHEAD
+#pragma unroll
+    for (int p = 0; p < ND; p++) t[p] = t[p] - (BH + (uint64_t)(ND - 1 - p) * (BL + BH)) + th[(ND + p) * stride];
+    normalize<ND>(t);
+#pragma unroll
+    for (int p = 0; p < ND; p++) a[p] = digit_to_double(t[p]);
+#else
     carry = 0;
 #pragma unroll
     for (int p = 0; p < ND; p++) {
@@ -367,6 +424,7 @@ __host__ __device__ __forceinline__ void montsqr(double (&a)[ND], const double* 
         carry = v >> D;
         a[p] = digit_to_double(t[p]);
     }
+#endif
 }
 
 // r <- r - n if r >= n (digits, r < 2n); nu: n's digits as integers

@@ -26,7 +26,7 @@ def model(tmp_path_factory):
     if not os.path.exists(NVCC) and not shutil.which("nvcc"):
         pytest.skip("nvcc not available")
     exe = str(tmp_path_factory.mktemp("f64") / "f64_model")
-    subprocess.check_call([NVCC, "-O2", "-std=c++17", "-o", exe, SRC])
+    subprocess.check_call([NVCC, "-O2", "-std=c++17", *os.environ.get("F64_MODEL_FLAGS", "").split(), "-o", exe, SRC])
     p = subprocess.Popen([exe], stdin=subprocess.PIPE, stdout=subprocess.PIPE, text=True)
 
     def call(line):
@@ -111,3 +111,24 @@ def test_montsqr_f64_matches_definition(model, S):
         r = int(out, 16)
         assert r < 2 * n, "almost-Montgomery bound r < 2n"
         assert r % n == a * a * pow(R, -1, n) % n
+
+
+@pytest.mark.parametrize("nd", [20, 40, 80])
+def test_normalize_carry_lookahead(model, nd):
+    """normalize(): columns < 2^62 -> 52-bit digits of the same number (mod 2^(52 nd)),
+    incl. carries rippling through runs of all-ones digits and across the 64-column
+    mask word boundary (nd = 80)."""
+    rng = random.Random(nd)
+    M = (1 << 52) - 1
+    cases = [[0] * nd, [M] * nd, [M + 1] + [M] * (nd - 1), [(1 << 62) - 1] * nd]
+    for start in (0, 5, 62, 63, 64):
+        if start < nd:
+            c = [M] * nd
+            c[start] = M + 1                      # generate at `start`, then propagate to the top
+            cases.append(c)
+    for _ in range(40):
+        cases.append([rng.choice([rng.getrandbits(62), M, M + 1, rng.getrandbits(52), 0]) for _ in range(nd)])
+    for cols in cases:
+        want = sum(v << (52 * k) for k, v in enumerate(cols)) % (1 << (52 * nd))
+        got = int(model("Z %d %s" % (nd, " ".join("%x" % v for v in cols))), 16)
+        assert got == want

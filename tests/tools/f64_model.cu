@@ -115,13 +115,31 @@ static void run(char op, char** tok) {
     printf("\n");
 }
 
+// "Z <ND> v_0 ... v_{ND-1}" (hex columns < 2^62) -> normalize() digits (hex, top first)
+template <int ND>
+static void run_norm(char** tok) {
+    uint64_t t[ND];
+    for (int k = 0; k < ND; k++) t[k] = strtoull(tok[k], nullptr, 16);
+    normalize<ND>(t);
+    for (int k = ND - 1; k >= 0; k--) printf("%013llx", (unsigned long long)t[k]);
+    printf("\n");
+}
+
 int main() {
     fesetround(FE_TOWARDZERO);
-    char line[8192];
+    char line[65536];
     while (fgets(line, sizeof line, stdin)) {
-        char* tok[8];
+        char* tok[96];
         int nt = 0;
-        for (char* p = strtok(line, " \n"); p && nt < 8; p = strtok(nullptr, " \n")) tok[nt++] = p;
+        for (char* p = strtok(line, " \n"); p && nt < 96; p = strtok(nullptr, " \n")) tok[nt++] = p;
+        if (nt > 2 && tok[0][0] == 'Z') {
+            const int nd = atoi(tok[1]);
+            if (nd == 20) run_norm<20>(tok + 2);
+            else if (nd == 40) run_norm<40>(tok + 2);
+            else if (nd == 80) run_norm<80>(tok + 2);
+            fflush(stdout);
+            continue;
+        }
         if (nt < 3) continue;
         const int S = atoi(tok[1]);
         switch (S) {
