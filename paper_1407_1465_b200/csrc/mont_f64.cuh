@@ -43,7 +43,10 @@
 #endif
 
 #ifndef RSA_F64_LOOKAHEAD
-#define RSA_F64_LOOKAHEAD 0   // carry-lookahead normalisation (A/B)
+#define RSA_F64_LOOKAHEAD 0   // carry-lookahead normalisation at ND < 64 (A/B: 565K vs 591K at 2048)
+#endif
+#ifndef RSA_F64_LOOKAHEAD_BIG
+#define RSA_F64_LOOKAHEAD_BIG 1   // ... at ND >= 64 (A/B: 60.2K vs 56.5K at 4096)
 #endif
 #ifndef RSA_F64_MU
 #define RSA_F64_MU 1      // CIOS loop trips unrolled (A/B knob)
@@ -299,26 +302,26 @@ __host__ __device__ __forceinline__ void montmul(double (&a)[ND], BF b, const do
     }
     // remove the exponent fields and propagate carries: column p now carries
     // 2 BH + (ND-1-p) BETA (mod 2^64) on top of its true value
-#if RSA_F64_LOOKAHEAD
+    if constexpr ((ND >= 64) ? RSA_F64_LOOKAHEAD_BIG : RSA_F64_LOOKAHEAD) {
 #pragma unroll
-    for (int p = 0; p < ND; p++) t[p] -= 2 * BH + (uint64_t)(ND - 1 - p) * BETA;
-    normalize<ND>(t);
+        for (int p = 0; p < ND; p++) t[p] -= 2 * BH + (uint64_t)(ND - 1 - p) * BETA;
+        normalize<ND>(t);
 #pragma unroll
-    for (int p = 0; p < ND; p++) {
-        if constexpr (AIN) aslot[p * stride] = digit_to_double(t[p]);
-        else a[p] = digit_to_double(t[p]);
+        for (int p = 0; p < ND; p++) {
+            if constexpr (AIN) aslot[p * stride] = digit_to_double(t[p]);
+            else a[p] = digit_to_double(t[p]);
+        }
+    } else {
+        uint64_t carry = 0;
+#pragma unroll
+        for (int p = 0; p < ND; p++) {
+            const uint64_t v = t[p] - (2 * BH + (uint64_t)(ND - 1 - p) * BETA) + carry;
+            t[p] = v & M52;
+            carry = v >> D;
+            if constexpr (AIN) aslot[p * stride] = digit_to_double(t[p]);
+            else a[p] = digit_to_double(t[p]);
+        }
     }
-#else
-    uint64_t carry = 0;
-#pragma unroll
-    for (int p = 0; p < ND; p++) {
-        const uint64_t v = t[p] - (2 * BH + (uint64_t)(ND - 1 - p) * BETA) + carry;
-        t[p] = v & M52;
-        carry = v >> D;
-        if constexpr (AIN) aslot[p * stride] = digit_to_double(t[p]);
-        else a[p] = digit_to_double(t[p]);
-    }
-#endif
 }
 
 // A <- A^2 R^-1 (mod n), result < 2n for A < 2n (squarings are ~85% of a
@@ -409,22 +412,22 @@ __host__ __device__ __forceinline__ void montsqr(double (&a)[ND], const double* 
         bias0 += BL + BH;
     }
     // 3. + T_high, normalise (column p carries BH + (ND-1-p)(BL+BH))
-#if RSA_F64_LOOKAHEAD
+    if constexpr ((ND >= 64) ? RSA_F64_LOOKAHEAD_BIG : RSA_F64_LOOKAHEAD) {
 #pragma unroll
-    for (int p = 0; p < ND; p++) t[p] = t[p] - (BH + (uint64_t)(ND - 1 - p) * (BL + BH)) + th[(ND + p) * stride];
-    normalize<ND>(t);
+        for (int p = 0; p < ND; p++) t[p] = t[p] - (BH + (uint64_t)(ND - 1 - p) * (BL + BH)) + th[(ND + p) * stride];
+        normalize<ND>(t);
 #pragma unroll
-    for (int p = 0; p < ND; p++) a[p] = digit_to_double(t[p]);
-#else
-    carry = 0;
+        for (int p = 0; p < ND; p++) a[p] = digit_to_double(t[p]);
+    } else {
+        carry = 0;
 #pragma unroll
-    for (int p = 0; p < ND; p++) {
-        const uint64_t v = t[p] - (BH + (uint64_t)(ND - 1 - p) * (BL + BH)) + th[(ND + p) * stride] + carry;
-        t[p] = v & M52;
-        carry = v >> D;
-        a[p] = digit_to_double(t[p]);
+        for (int p = 0; p < ND; p++) {
+            const uint64_t v = t[p] - (BH + (uint64_t)(ND - 1 - p) * (BL + BH)) + th[(ND + p) * stride] + carry;
+            t[p] = v & M52;
+            carry = v >> D;
+            a[p] = digit_to_double(t[p]);
+        }
     }
-#endif
 }
 
 // r <- r - n if r >= n (digits, r < 2n); nu: n's digits as integers
