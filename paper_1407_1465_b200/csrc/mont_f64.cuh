@@ -45,11 +45,14 @@
 #ifndef RSA_F64_LOOKAHEAD
 #define RSA_F64_LOOKAHEAD 0   // carry-lookahead normalisation at ND < 64 (A/B: 565K vs 591K at 2048)
 #endif
+#ifndef RSA_F64_LOOKAHEAD_SMALL
+#define RSA_F64_LOOKAHEAD_SMALL 0   // ... at ND <= 20 (A/B: CRT-2048 2.04M vs 2.19M)
+#endif
 #ifndef RSA_F64_LOOKAHEAD_BIG
 #define RSA_F64_LOOKAHEAD_BIG 1   // ... at ND >= 64 (A/B: 60.2K vs 56.5K at 4096)
 #endif
 #ifndef RSA_F64_MU
-#define RSA_F64_MU 1      // CIOS loop trips unrolled (A/B knob)
+#define RSA_F64_MU 1      // CIOS loop trips unrolled (A/B: 2 -> 561K vs 565K at 2048, 37.4K vs 60.2K at 4096)
 #endif
 #ifndef RSA_F64_RU
 #define RSA_F64_RU 4      // squaring's reduction loop trips unrolled at ND >= 40 (A/B knob:
@@ -302,7 +305,7 @@ __host__ __device__ __forceinline__ void montmul(double (&a)[ND], BF b, const do
     }
     // remove the exponent fields and propagate carries: column p now carries
     // 2 BH + (ND-1-p) BETA (mod 2^64) on top of its true value
-    if constexpr ((ND >= 64) ? RSA_F64_LOOKAHEAD_BIG : RSA_F64_LOOKAHEAD) {
+    if constexpr ((ND >= 64) ? RSA_F64_LOOKAHEAD_BIG : (ND <= 20 ? RSA_F64_LOOKAHEAD_SMALL : RSA_F64_LOOKAHEAD)) {
 #pragma unroll
         for (int p = 0; p < ND; p++) t[p] -= 2 * BH + (uint64_t)(ND - 1 - p) * BETA;
         normalize<ND>(t);
@@ -412,7 +415,7 @@ __host__ __device__ __forceinline__ void montsqr(double (&a)[ND], const double* 
         bias0 += BL + BH;
     }
     // 3. + T_high, normalise (column p carries BH + (ND-1-p)(BL+BH))
-    if constexpr ((ND >= 64) ? RSA_F64_LOOKAHEAD_BIG : RSA_F64_LOOKAHEAD) {
+    if constexpr ((ND >= 64) ? RSA_F64_LOOKAHEAD_BIG : (ND <= 20 ? RSA_F64_LOOKAHEAD_SMALL : RSA_F64_LOOKAHEAD)) {
 #pragma unroll
         for (int p = 0; p < ND; p++) t[p] = t[p] - (BH + (uint64_t)(ND - 1 - p) * (BL + BH)) + th[(ND + p) * stride];
         normalize<ND>(t);
