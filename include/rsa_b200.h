@@ -88,9 +88,9 @@ int rsa_validate_key(const uint32_t* e, const uint32_t* d, const uint32_t* p,
  *               workspace allocation) and returns; completion is observed
  *               through the stream.  count == 0 is a no-op returning RSA_OK.
  * Kernels (results identical; chosen by measurement): moduli of
- * 1025..4096 bits run on the FP64 pipe (52-bit digits, exact DFMA.RZ products);
+ * 513..4096 bits run on the FP64 pipe (52-bit digits, exact DFMA.RZ products);
  * narrower ones, and these too with the environment variables RSA_B200_F64=0
- * (1024/2048-bit classes) or RSA_B200_F64_4096=0, on the integer (IMAD) pipe.
+ * (513..2048 bits) or RSA_B200_F64_4096=0 (2049..4096), on the integer (IMAD) pipe.
  * Errors: RSA_EINVAL, RSA_ERANGE, RSA_EEVEN, RSA_ECUDA. */
 int rsa_modexp_batch(const uint32_t* base, const uint32_t* exp, const uint32_t* n,
                      int nbits, size_t count, uint32_t* out, void* stream);
