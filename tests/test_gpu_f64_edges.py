@@ -37,7 +37,7 @@ def moduli(nb):
     ]
 
 
-@pytest.mark.parametrize("nb", [1025, 1536, 2047, 2048, 2049, 3072, 4095, 4096])
+@pytest.mark.parametrize("nb", [513, 1000, 1024, 1025, 1536, 2047, 2048, 2049, 3072, 4095, 4096])
 def test_f64_edge_moduli(R, nb):
     rnd = random.Random(52 * nb)
     s = workload.limbs_needed(nb)
