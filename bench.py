@@ -491,7 +491,7 @@ def run_ours(args, rank, world, local_rank):
         cpu = cpu_baseline(key, base_np, legs, args.cpu_seconds)
     line = {"metric": METRIC, "value": value, "unit": "modexp/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
-            "vs_baseline": None, "dtype": "u32", "data": "synthetic",
+            "vs_baseline": None, "dtype": "f64" if fp64 else "u32", "data": "synthetic",
             "config": {"workload": args.config, "packets_per_rank": count, "key": key_name + " (seeded, "
                        "workload/keys.json)", "legs": [l for l, _ in legs], "modulus_bits": nb,
                        "l2": f"inputs {count * s * 4 / 2**20:.0f} MiB per leg vs 126 MB L2"
