@@ -58,7 +58,7 @@
 #define RSA_F64_RU 4      // squaring's reduction loop trips unrolled at ND >= 40 (A/B knob:
 #endif                    // 1/2/4/5 -> 565K/581K/590K/585K RSA-2048 decrypts/s)
 #ifndef RSA_F64_RU_SMALL
-#define RSA_F64_RU_SMALL 1   // ... at ND < 40
+#define RSA_F64_RU_SMALL 1   // ... at ND < 40 (A/B, CRT-2048: 1/2/4 -> 2.19M/2.14M/1.87M)
 #endif
 
 namespace rsa_b200 {
