@@ -198,6 +198,22 @@ def measured_dfma_rate():
     return best
 
 
+def measured_digit_mix_rate():
+    """Best FP64 ops/clk/SM of the digit-product instruction mix (DFMA.RZ, DADD,
+    DFMA.RZ + a 64-bit column add) in profiles/r01_dfma_latency.jsonl, or None."""
+    best = None
+    try:
+        with open(os.path.join(ROOT, "profiles", "r01_dfma_latency.jsonl")) as f:
+            for line in f:
+                if line.startswith("{"):
+                    v = json.loads(line).get("fp64_ops_per_clk_per_sm")
+                    if v is not None:
+                        best = v if best is None or v > best else best
+    except (OSError, ValueError):
+        return None
+    return best
+
+
 def batch_kernel_name(S: int, fp64: bool = False) -> str:
     """The kernel modexp.cu launches for width class S (same env switches)."""
     if fp64:
@@ -458,6 +474,9 @@ def run_ours(args, rank, world, local_rank):
                           f"(MEASURED_PEAKS sm_max_mhz)",
             **({"peak_measured_dfma": dfma * sms * f_max * 1e6 / 1e12,
                 "frac_of_measured_dfma": f_ach / (dfma * sms * f_max * 1e6 / 1e12)} if dfma else {}),
+            **({"peak_measured_digit_mix": mix * sms * f_max * 1e6 / 1e12,
+                "frac_of_measured_digit_mix": f_ach / (mix * sms * f_max * 1e6 / 1e12)}
+               if (mix := measured_digit_mix_rate()) else {}),
             "imad_equiv": {"achieved": achieved, "peak": peak, "unit": "Tprod/s", "frac": achieved / peak,
                            "basis": "the path's 32x32->64 limb-product count (the metric's '% of IMAD peak') "
                                     "against 32 products/clk/SM on the integer pipe"}})

@@ -37,7 +37,7 @@ def build(force: bool = False, verbose: bool = False, out: str | None = None) ->
     subprocess.check_call(cmd)
     os.replace(LIB + ".tmp", LIB)
     # the microbenchmarks (roofline denominator, chain latency), built alongside
-    for name in ("imad_peak", "imad_latency"):
+    for name in ("imad_peak", "imad_latency", "dfma_latency"):
         mb = os.path.join(CSRC, "microbench", name)
         src = mb + ".cu"
         if os.path.exists(src) and (force or not os.path.exists(mb) or os.path.getmtime(mb) < os.path.getmtime(src)):
