@@ -11,7 +11,7 @@
 
 constexpr int ITERS = 2048;
 
-template <int C>
+template <int C, int MODE>   // MODE 0: the kernel's mix; 1: without the 64-bit column adds
 __global__ void chain_kernel(unsigned long long* out, double x0, unsigned long long* clk) {
     double x[C], y = 1234567.0 + threadIdx.x;
     unsigned long long acc[C];
@@ -24,7 +24,8 @@ __global__ void chain_kernel(unsigned long long* out, double x0, unsigned long l
         for (int c = 0; c < C; c++) {
             const double h = __fma_rz(x[c], y, c104);
             const double l = __fma_rz(x[c], y, __dsub_rn(c2, h));
-            acc[c] += (unsigned long long)__double_as_longlong(l) + (unsigned long long)__double_as_longlong(h);
+            if (MODE == 0)
+                acc[c] += (unsigned long long)__double_as_longlong(l) + (unsigned long long)__double_as_longlong(h);
             // the next product of this chain depends on this one: x <- l (an integer
             // in [2^52, 2^53); with y < 2^21 the product stays < 2^104, the split exact)
             x[c] = l;
@@ -33,31 +34,32 @@ __global__ void chain_kernel(unsigned long long* out, double x0, unsigned long l
     const long long t1 = clock64();
     unsigned long long s = 0;
 #pragma unroll
-    for (int c = 0; c < C; c++) s += acc[c];
+    for (int c = 0; c < C; c++) s += acc[c] + (unsigned long long)__double_as_longlong(x[c]);
     out[blockIdx.x * blockDim.x + threadIdx.x] = s;
     if (blockIdx.x == 0 && threadIdx.x == 0) clk[0] = (unsigned long long)(t1 - t0);
 }
 
-template <int C>
+template <int C, int MODE = 0>
 static int run(int sms, int w) {
     unsigned long long *out, *clk;
     const int block = 128 * w;   // W warps per SMSP
     cudaMalloc(&out, sizeof(unsigned long long) * sms * block);
     cudaMalloc(&clk, sizeof(unsigned long long));
-    chain_kernel<C><<<sms, block>>>(out, 3.0, clk);
+    chain_kernel<C, MODE><<<sms, block>>>(out, 3.0, clk);
     cudaDeviceSynchronize();
     double best = 1e30;
     for (int r = 0; r < 3; r++) {
-        chain_kernel<C><<<sms, block>>>(out, 3.0, clk);
+        chain_kernel<C, MODE><<<sms, block>>>(out, 3.0, clk);
         cudaDeviceSynchronize();
         unsigned long long c = 0;
         cudaMemcpy(&c, clk, sizeof c, cudaMemcpyDeviceToHost);
         if (c < best) best = (double)c;
     }
     const double products = (double)ITERS * C;   // per warp
-    printf("{\"chains_per_thread\": %d, \"warps_per_smsp\": %d, \"cycles_per_product_per_warp\": %.2f, "
-           "\"fp64_ops_per_clk_per_sm\": %.1f}\n",
-           C, w, best / products, 3.0 * products * 32 * 4 * w / best);
+    printf("{\"mix\": \"%s\", \"chains_per_thread\": %d, \"warps_per_smsp\": %d, "
+           "\"cycles_per_product_per_warp\": %.2f, \"fp64_ops_per_clk_per_sm\": %.1f}\n",
+           MODE == 0 ? "dfma+dadd+dfma+iadd3x2" : "dfma+dadd+dfma", C, w, best / products,
+           3.0 * products * 32 * 4 * w / best);
     cudaFree(out);
     cudaFree(clk);
     return 0;
@@ -69,5 +71,6 @@ int main() {
     for (int w : {1, 2, 4}) {
         run<1>(sms, w); run<2>(sms, w); run<4>(sms, w); run<8>(sms, w);
     }
+    for (int w : {2, 4}) { run<2, 1>(sms, w); run<4, 1>(sms, w); run<8, 1>(sms, w); }
     return 0;
 }
