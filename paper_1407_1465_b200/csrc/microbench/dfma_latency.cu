@@ -11,8 +11,10 @@
 
 constexpr int ITERS = 2048;
 
-template <int C, int MODE>   // MODE 0: the kernel's mix; 1: without the 64-bit column adds
-__global__ void chain_kernel(unsigned long long* out, double x0, unsigned long long* clk) {
+// MODE 0: the kernel's mix; 1: without the 64-bit column adds; 2: the column adds as
+// add.cc (IADD3, ALU) + madc by a runtime 1 (IMAD.X, the IMAD pipe) for the high words
+template <int C, int MODE>
+__global__ void chain_kernel(unsigned long long* out, double x0, unsigned long long* clk, unsigned one) {
     double x[C], y = 1234567.0 + threadIdx.x;
     unsigned long long acc[C];
 #pragma unroll
@@ -24,8 +26,18 @@ __global__ void chain_kernel(unsigned long long* out, double x0, unsigned long l
         for (int c = 0; c < C; c++) {
             const double h = __fma_rz(x[c], y, c104);
             const double l = __fma_rz(x[c], y, __dsub_rn(c2, h));
-            if (MODE == 0)
+            if (MODE == 0) {
                 acc[c] += (unsigned long long)__double_as_longlong(l) + (unsigned long long)__double_as_longlong(h);
+            } else if (MODE == 2) {
+                const unsigned long long bl = __double_as_longlong(l), bh = __double_as_longlong(h);
+                unsigned lo = (unsigned)acc[c], hi = (unsigned)(acc[c] >> 32);
+                asm volatile("add.cc.u32 %0, %0, %2;\n\tmadc.lo.u32 %1, %3, %6, %1;\n\t"
+                             "add.cc.u32 %0, %0, %4;\n\tmadc.lo.u32 %1, %5, %6, %1;"
+                             : "+r"(lo), "+r"(hi)
+                             : "r"((unsigned)bl), "r"((unsigned)(bl >> 32)), "r"((unsigned)bh),
+                               "r"((unsigned)(bh >> 32)), "r"(one));
+                acc[c] = ((unsigned long long)hi << 32) | lo;
+            }
             // the next product of this chain depends on this one: x <- l (an integer
             // in [2^52, 2^53); with y < 2^21 the product stays < 2^104, the split exact)
             x[c] = l;
@@ -45,11 +57,11 @@ static int run(int sms, int w) {
     const int block = 128 * w;   // W warps per SMSP
     cudaMalloc(&out, sizeof(unsigned long long) * sms * block);
     cudaMalloc(&clk, sizeof(unsigned long long));
-    chain_kernel<C, MODE><<<sms, block>>>(out, 3.0, clk);
+    chain_kernel<C, MODE><<<sms, block>>>(out, 3.0, clk, 1u);
     cudaDeviceSynchronize();
     double best = 1e30;
     for (int r = 0; r < 3; r++) {
-        chain_kernel<C, MODE><<<sms, block>>>(out, 3.0, clk);
+        chain_kernel<C, MODE><<<sms, block>>>(out, 3.0, clk, 1u);
         cudaDeviceSynchronize();
         unsigned long long c = 0;
         cudaMemcpy(&c, clk, sizeof c, cudaMemcpyDeviceToHost);
@@ -58,7 +70,8 @@ static int run(int sms, int w) {
     const double products = (double)ITERS * C;   // per warp
     printf("{\"mix\": \"%s\", \"chains_per_thread\": %d, \"warps_per_smsp\": %d, "
            "\"cycles_per_product_per_warp\": %.2f, \"fp64_ops_per_clk_per_sm\": %.1f}\n",
-           MODE == 0 ? "dfma+dadd+dfma+iadd3x2" : "dfma+dadd+dfma", C, w, best / products,
+           MODE == 0 ? "dfma+dadd+dfma+iadd3x2" : (MODE == 1 ? "dfma+dadd+dfma" : "dfma+dadd+dfma+(iadd3+imad.x)x2"),
+           C, w, best / products,
            3.0 * products * 32 * 4 * w / best);
     cudaFree(out);
     cudaFree(clk);
@@ -72,5 +85,6 @@ int main() {
         run<1>(sms, w); run<2>(sms, w); run<4>(sms, w); run<8>(sms, w);
     }
     for (int w : {2, 4}) { run<2, 1>(sms, w); run<4, 1>(sms, w); run<8, 1>(sms, w); }
+    for (int w : {2, 4}) { run<2, 2>(sms, w); run<4, 2>(sms, w); run<8, 2>(sms, w); }
     return 0;
 }
