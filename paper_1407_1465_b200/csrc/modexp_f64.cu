@@ -6,13 +6,15 @@
 // warp-uniformly.  The Montgomery multiply is mont_f64.cuh: 52-bit digits in
 // doubles, products split exactly by DFMA.RZ, column sums in 64-bit integers.
 //
-// Per thread: A (ND doubles) and the CIOS accumulator (ND 64-bit columns) in
-// registers; the b operand streams from this thread's shared-memory slot
-// (digit-major across the block: conflict-free LDS.64); n's digits are
-// constant-bank operands of the DFMAs.  The window table holds entries as
-// digit pairs (double2), entry-major then digit-pair-major across the grid's
-// threads (coalesced).  Intermediates stay < 2n (R = 2^(52 ND) > 4n), and one
-// subtraction canonicalises the result before the store.
+// Per thread (S = 32, 64): A (ND doubles) and the accumulator (ND 64-bit
+// columns) in registers; a 2 ND-digit shared-memory slot (digit-major across
+// the block: conflict-free LDS.64) holds the b operand and A while a multiply
+// runs (A re-read per digit), or the square's 2 ND digits.  S = 128: A lives
+// in an ND-digit slot and b is read in place (see F64Cfg::ONESLOT).  n's digits
+// come from one per-block shared copy (volatile pair loads).  The window table
+// holds entries as digit pairs (double2), entry-major then digit-pair-major
+// across the grid's threads (coalesced).  Intermediates stay < 2n
+// (R = 2^(52 ND) > 4n), and one subtraction canonicalises the result.
 #include <cuda_runtime.h>
 #include <stdint.h>
 

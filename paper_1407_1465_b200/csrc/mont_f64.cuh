@@ -19,16 +19,20 @@
 // carry chains: a column of the CIOS accumulator receives 4 terms < 2^52 per
 // iteration and lives <= ND iterations, so its true value stays < 2^60.
 //
-// Why: on B200 the DFMA pipe issues ~53 results/clk/SM (profiles/
-// r01_imad_peak.jsonl) and one 52x52 product costs 3 FP64 ops (DFMA, DADD,
-// DFMA) -> ~17.7 products x 2704 bit^2 per clk, against ~28 IMAD.WIDE.X
-// products x 1024 bit^2 on the integer pipe: 1.66x the multiply throughput.
+// Why: on B200 the DFMA pipe issues ~53-64 results/clk/SM (profiles/
+// r01_imad_peak.jsonl, r01_dfma_latency.jsonl) and one 52x52 product costs 3
+// FP64 ops (DFMA, DADD, DFMA) + one 64-bit add: the measured mix sustains ~41
+// FP64 ops/clk/SM = ~13.7 products x 2704 bit^2 per clk, against ~28
+// IMAD.WIDE.X products x 1024 bit^2 on the integer pipe: ~1.3x the multiply
+// throughput (the RSA kernels: +13% at 2048 bits, +24% at 4096).
 //
 // CIOS (operand scanning) with R = 2^(52 ND), for i = 0 .. ND-1:
 //   T += A b_i ;  q = T_0 n' mod 2^52 ;  T += q n ;  T /= 2^52
 // The division is a register rename folded into the adds: column j of the
 // new T is written from column j+1 of the old one (t[j-1] = t[j] + ...), in
-// place, so a loop iteration needs no moves and no unrolling.
+// place, so a loop iteration needs no moves and no unrolling.  montsqr is the
+// squaring (product scan + reduction loop), normalize the carry-lookahead
+// end-of-op normalisation (used at ND >= 64).
 //
 // Bounds: A, B < 2n and 4n < R give T < 2n (almost-Montgomery: no
 // subtraction inside the exponentiation; the caller canonicalises once at the
