@@ -55,6 +55,9 @@
 #ifndef RSA_F64_LOOKAHEAD_BIG
 #define RSA_F64_LOOKAHEAD_BIG 1   // ... at ND >= 64 (A/B: 60.2K vs 56.5K at 4096)
 #endif
+#ifndef RSA_F64_NREG
+#define RSA_F64_NREG 0   // A/B: n in registers in the reduction loop, 552K vs 591K at 2048 (CRT-2048 even)
+#endif
 #ifndef RSA_F64_MU
 #define RSA_F64_MU 1      // CIOS loop trips unrolled (A/B: 2 -> 561K vs 565K at 2048, 37.4K vs 60.2K at 4096)
 #endif
@@ -391,12 +394,23 @@ __host__ __device__ __forceinline__ void montsqr(double (&a)[ND], const double* 
     // chain) is computed there and overlaps the remaining ND-2 products.
     uint64_t bias0 = BL;
     double qd = digit_to_double(((t[0] & M52) * np) & M52);
+    // RSA_F64_NREG: n's digits held in registers for the loop (A's registers are
+    // free here) instead of ND/2 shared-memory pair loads per iteration (A/B)
+    double nr[RSA_F64_NREG ? ND : 2];
+    if constexpr (RSA_F64_NREG != 0) {
+#pragma unroll
+        for (int g = 0; g < ND / 2; g++) nd_pair(nd, g, nr[2 * g], nr[2 * g + 1]);
+    }
+    auto npair = [&](int g, double& x, double& y) {
+        if constexpr (RSA_F64_NREG != 0) { x = nr[2 * g]; y = nr[2 * g + 1]; }
+        else nd_pair(nd, g, x, y);
+    };
 #ifdef __CUDA_ARCH__
 #pragma unroll RU
 #endif
     for (int i = 0; i < ND; i++) {
         double n0, n1;
-        nd_pair(nd, 0, n0, n1);
+        npair(0, n0, n1);
         const double hq0 = fma_rz(qd, n0, c104);
         const double lq0 = fma_rz(qd, n0, sub_rn(C2, hq0));
         const uint64_t cr = (t[0] + bits(lq0) - bias0) >> D;   // column 0 is 0 mod 2^52
@@ -408,7 +422,7 @@ __host__ __device__ __forceinline__ void montsqr(double (&a)[ND], const double* 
 #pragma unroll
         for (int j = 2; j < ND; j++) {
             double nj = n1;
-            if ((j & 1) == 0) nd_pair(nd, j / 2, nj, n1);
+            if ((j & 1) == 0) npair(j / 2, nj, n1);
             const double h = fma_rz(qd, nj, c104);
             const double l = fma_rz(qd, nj, sub_rn(C2, h));
             t[j - 1] = t[j] + bits(l) + hqp;
