@@ -35,6 +35,9 @@ namespace rsa_b200 {
 #ifndef RSA_F64_FUSEJ
 #define RSA_F64_FUSEJ 0     // 4096-bit kernel: one fused j-loop (A/B: 54.4K vs 56.4K, no spills but less overlap)
 #endif
+#ifndef RSA_F64_SQRSMEM
+#define RSA_F64_SQRSMEM 0   // 4096-bit kernel: separate squaring instance with LDS b reads (A/B: 56.6K vs 60.2K)
+#endif
 #ifndef RSA_F64_FUSEJ64
 #define RSA_F64_FUSEJ64 0   // 1024/2048-bit multiply: fused j-loop (A/B)
 #endif
@@ -157,9 +160,18 @@ modexp_f64_kernel(const __grid_constant__ ModexpF64Params<S> p) {
                 } else if (op.kind == RSA_OP_R2) { bp = cst; P = 2; Q = 1; }
                 else { bp = cst + ND; P = 2; Q = 1; }   // RSA_OP_ONE (plans for this class carry no MULX)
                 auto bget = [&](int i) -> double { return bp[(size_t)(i >> 1) * P + (i & 1) * Q]; };
-                for (int r = 0; r < op.rep; r++)
-                    f64::montmul<ND, true, decltype(bget), true, RSA_F64_FUSEJ>(a, bget, nds, p.np52, p.c104, t, bsm,
-                                                                              stride);
+                if (RSA_F64_SQRSMEM && op.kind == RSA_OP_SQR) {
+                    // squarings (the bulk): b is the slot itself, read with explicit
+                    // shared-memory loads instead of generic ones
+                    auto bsq = [&](int i) -> double { return f64::ld_digit(bsm + (size_t)i * stride); };
+                    for (int r = 0; r < op.rep; r++)
+                        f64::montmul<ND, true, decltype(bsq), true, RSA_F64_FUSEJ>(a, bsq, nds, p.np52, p.c104, t,
+                                                                                  bsm, stride);
+                } else {
+                    for (int r = 0; r < op.rep; r++)
+                        f64::montmul<ND, true, decltype(bget), true, RSA_F64_FUSEJ>(a, bget, nds, p.np52, p.c104, t,
+                                                                                   bsm, stride);
+                }
             } else
             for (int r = 0; r < op.rep; r++) {
                 if constexpr (F64Cfg<S>::LOCKSTEP) __syncthreads();

@@ -396,7 +396,7 @@ __host__ __device__ __forceinline__ void montsqr(double (&a)[ND], const double* 
     double qd = digit_to_double(((t[0] & M52) * np) & M52);
     // RSA_F64_NREG: n's digits held in registers for the loop (A's registers are
     // free here) instead of ND/2 shared-memory pair loads per iteration (A/B)
-    double nr[RSA_F64_NREG ? ND : 2];
+    [[maybe_unused]] double nr[RSA_F64_NREG ? ND : 2];
     if constexpr (RSA_F64_NREG != 0) {
 #pragma unroll
         for (int g = 0; g < ND / 2; g++) nd_pair(nd, g, nr[2 * g], nr[2 * g + 1]);
