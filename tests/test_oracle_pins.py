@@ -56,6 +56,32 @@ def test_p1_fig12_halving_loop():
     assert oracle.modexp(5, 0, 7) == 1
 
 
+@pytest.mark.parametrize("m", [1, 2, 3, 7, 497, 17947, 513581, 65537, 2**31 - 1, 2**30 + 3, 1000000006])
+def test_p11_fig12_halving_every_exponent(m):
+    """Fig 12 computes (g^2)^floor(e/2) * g^(e mod 2) mod m:
+    pinned to CPython pow (an independent library routine) for every exponent
+    0..300, both parities, bases below and above m (g % den first),
+    so a wrong even-e or odd-e branch fails here, not only on the GPU."""
+    rng = random.Random(m)
+    bases = [0, 1, 2, m - 1, m, m + 1, rng.randrange(m), rng.randrange(2**32), 2**40 + 17]
+    for g in bases:
+        g = max(g, 0)
+        for e in range(0, 301):
+            want = pow(g, e, m)
+            assert oracle.halving(g, e, m, faithful=False) == want, (g, e, m)
+            # faithful mode differs only at e = 0 (reading Z5: returns g % den)
+            assert oracle.halving(g, e, m, faithful=True) == (g % m if e == 0 else want), (g, e, m)
+
+
+def test_p11_fig12_halving_large_exponents():
+    rng = random.Random(1212)
+    for _ in range(200):
+        m = rng.randrange(2, 2**31)
+        g = rng.randrange(2**40)
+        e = rng.randrange(1, 2**20)
+        assert oracle.halving(g, e, m, faithful=True) == pow(g, e, m)
+
+
 # ------------------------------------------------------------------ P2
 
 def test_p2_fig2_key():
