@@ -207,6 +207,39 @@ int rsa_multi_plan_info(int nbits, int exp_bits, int mr, rsa_plan_info_t* info);
  * (0 = automatic, the default; 1..7 = fixed).  For tests and benchmarks. */
 int rsa_set_window(int w);
 
+/* ---- kernel path per width class (measurement and A/B only) -----------
+ * A batch of an nbits-bit modulus runs in width class S = the smallest of
+ * 2, 4, 8, 16, 32, 64, 128 limbs >= ceil(nbits/32).  Each class runs, by
+ * default, the kernel measured fastest on B200 (DESIGN.md "Shapes chosen by
+ * measurement"); every path computes the same, bit-exact result (the Montgomery
+ * multiply of Fig 3), only the number representation and the
+ * thread shape differ.  Paths:
+ *   RSA_PATH_DEFAULT    the measured default of the class (see below)
+ *   RSA_PATH_FP64       S = 32, 64, 128: 52-bit digits on the FP64 pipe
+ *                       (default for those classes)
+ *   RSA_PATH_INT        32-bit limbs, IMAD carry chains, one thread per packet
+ *                       (default for S = 8, 16; for S = 128 it means the
+ *                       2-lane pair kernel)
+ *   RSA_PATH_INT_GROUP  S = 64: 2 lanes per packet; S = 128: 4 lanes
+ *   RSA_PATH_INT_PAIR   S = 128: 2 lanes per packet
+ *   RSA_PATH_INT_MULTI  S = 2, 4: several packets per thread (default there)
+ * rsa_set_kernel_path sets the path of class `width_class` for subsequent
+ * calls of every thread (process-wide, thread-safe; a call in flight keeps the
+ * path it started with).  RSA_PATH_DEFAULT restores the default, under which
+ * the RSA_B200_F64 / _F64_4096 / _SHAPE64 / _TPI128 / _SMALL environment
+ * switches of the A/B tools are honoured (read per call).
+ * Errors: RSA_EINVAL (no such class, or the class has no such kernel).
+ * rsa_get_kernel_path returns the path the class resolves to now (never
+ * RSA_PATH_DEFAULT), or RSA_EINVAL for an unknown class. */
+#define RSA_PATH_DEFAULT    0
+#define RSA_PATH_FP64       1
+#define RSA_PATH_INT        2
+#define RSA_PATH_INT_GROUP  3
+#define RSA_PATH_INT_PAIR   4
+#define RSA_PATH_INT_MULTI  5
+int rsa_set_kernel_path(int width_class, int path);
+int rsa_get_kernel_path(int width_class);
+
 /* ---- packet codec: sec. 2, PAPER.md:39-40 -----------------------------
  * rsa_encode: strips ASCII spaces, maps a=00 .. z=25 and packs consecutive
  * letter pairs as hi*100 + lo ("parallel encryption" ->

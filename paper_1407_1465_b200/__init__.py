@@ -36,7 +36,10 @@ EXPORTS = ["rsa_strerror", "rsa_keygen_check", "rsa_validate_key", "rsa_modexp_b
            "rsa_modexp_batch_host", "rsa_plan_info", "rsa_set_window", "rsa_encode", "rsa_decode",
            "rsa_kernel_launches", "rsa_modexp_batch_paper", "rsa_modexp_batch_multi", "rsa_miller_rabin_batch",
            "rsa_prime_candidates", "rsa_prime_sieve", "rsa_prime_search", "rsa_keygen", "rsa_multi_plan_info",
-           "rsa_decrypt_crt_batch", "rsa_encrypt_text", "rsa_decrypt_text"]
+           "rsa_decrypt_crt_batch", "rsa_encrypt_text", "rsa_decrypt_text", "rsa_set_kernel_path",
+           "rsa_get_kernel_path"]
+# kernel paths per width class (rsa_set_kernel_path; include/rsa_b200.h)
+RSA_PATH_DEFAULT, RSA_PATH_FP64, RSA_PATH_INT, RSA_PATH_INT_GROUP, RSA_PATH_INT_PAIR, RSA_PATH_INT_MULTI = range(6)
 
 if not os.path.exists(LIB_PATH):
     raise ImportError(f"{LIB_PATH} is not built: run `python paper_1407_1465_b200/build.py` "
@@ -64,6 +67,8 @@ _lib.rsa_modexp_batch_host.argtypes = [ctypes.c_void_p, _u32p, _u32p, ctypes.c_i
                                        ctypes.c_void_p]
 _lib.rsa_plan_info.argtypes = [_u32p, _u32p, ctypes.c_int, ctypes.POINTER(RsaPlanInfo)]
 _lib.rsa_set_window.argtypes = [ctypes.c_int]
+_lib.rsa_set_kernel_path.argtypes = [ctypes.c_int, ctypes.c_int]
+_lib.rsa_get_kernel_path.argtypes = [ctypes.c_int]
 _lib.rsa_encode.argtypes = [ctypes.c_char_p, _u32p, ctypes.c_size_t, ctypes.POINTER(ctypes.c_size_t)]
 _lib.rsa_decode.argtypes = [_u32p, ctypes.c_size_t, ctypes.c_char_p, ctypes.c_size_t]
 _lib.rsa_kernel_launches.restype = ctypes.c_ulonglong
@@ -120,6 +125,35 @@ def _on(device):
     return torch.cuda.device(device)
 
 
+def _rows(t, s: int, name: str, cuda: bool = True, like=None):
+    """Check a packet array at the boundary: 2-D [count, s], 4-byte elements,
+    C-contiguous, on a CUDA device (cuda=True) or in host memory (cuda=False),
+    and shaped like `like` if given.  The C side trusts count*s, so a wrong
+    shape here would be an out-of-bounds access there."""
+    import torch
+    if isinstance(t, np.ndarray):
+        ok = (not cuda and t.ndim == 2 and t.shape[1] == s and t.itemsize == 4 and t.flags.c_contiguous)
+    elif isinstance(t, torch.Tensor):
+        ok = (t.dim() == 2 and t.shape[1] == s and t.element_size() == 4 and t.is_contiguous()
+              and t.is_cuda == cuda and not (t.dtype.is_floating_point or t.dtype.is_complex))
+    else:
+        ok = False
+    if ok and like is not None:
+        ok = tuple(t.shape) == tuple(like.shape) and (not cuda or t.device == like.device)
+    if not ok:
+        where = "CUDA" if cuda else "host (numpy or CPU tensor)"
+        shape = f"[{like.shape[0]}, {s}]" if like is not None else f"[count, {s}]"
+        raise ValueError(f"{name} must be a contiguous {where} {shape} array of 32-bit integers")
+    return t
+
+
+def _vec(t, n: int, name: str, itemsize: int, cuda: bool = True):
+    """A contiguous 1-D CUDA tensor of n elements of `itemsize` bytes."""
+    if t.dim() != 1 or t.numel() != n or t.element_size() != itemsize or not t.is_contiguous() or t.is_cuda != cuda:
+        raise ValueError(f"{name} must be a contiguous 1-D CUDA tensor of {n} {8 * itemsize}-bit elements")
+    return t
+
+
 def to_int(a) -> int:
     return int.from_bytes(np.ascontiguousarray(a, dtype="<u4").tobytes(), "little")
 
@@ -144,13 +178,10 @@ def rsa_modexp_batch(base, exp: int, n: int, nbits: int, out=None, stream=None):
     """
     import torch
     s = nlimbs(nbits)
-    if base.dim() != 2 or base.shape[1] != s or not base.is_cuda or base.element_size() != 4:
-        raise ValueError(f"base must be a CUDA [count, {s}] 32-bit tensor")
-    base = base.contiguous()
+    base = _rows(base.contiguous() if isinstance(base, torch.Tensor) else base, s, "base")
     if out is None:
         out = torch.empty_like(base)
-    if out.shape != base.shape or not out.is_contiguous() or out.element_size() != 4:
-        raise ValueError("out must be a contiguous tensor shaped like base")
+    _rows(out, s, "out", like=base)
     if stream is None:
         stream = torch.cuda.current_stream(base.device).cuda_stream
     elif hasattr(stream, "cuda_stream"):
@@ -167,11 +198,10 @@ def rsa_decrypt_crt_batch(c, p: int, q: int, d: int, nbits: int, out=None, strea
     """M = c^d mod pq by the CRT (two half-width exponentiations + Garner)."""
     import torch
     s = nlimbs(nbits)
-    if c.dim() != 2 or c.shape[1] != s or not c.is_cuda:
-        raise ValueError(f"c must be a CUDA [count, {s}] tensor")
-    c = c.contiguous()
+    c = _rows(c.contiguous(), s, "c")
     if out is None:
         out = torch.empty_like(c)
+    _rows(out, s, "out", like=c)
     pl = nlimbs(max(p.bit_length(), q.bit_length(), 1))
     with _on(c.device):
         rc = _lib.rsa_decrypt_crt_batch(_vp(c.data_ptr()), _p(limbs(p, pl)), _p(limbs(q, pl)), pl, _p(limbs(d, s)),
@@ -187,8 +217,15 @@ def rsa_encrypt_text(text, e: int, n: int, nbits: int, status=None, out=None, st
     if isinstance(text, str):
         text = torch.tensor(list(text.replace(" ", "").encode("ascii")), dtype=torch.uint8, device="cuda")
     s = nlimbs(nbits)
+    if text.dim() != 1 or text.element_size() != 1 or not text.is_cuda or not text.is_contiguous():
+        raise ValueError("text must be a contiguous 1-D CUDA uint8 tensor")
     if out is None:
         out = torch.empty((text.numel() // 2, s), dtype=torch.int32, device=text.device)
+    _rows(out, s, "out")
+    if out.shape[0] != text.numel() // 2 or out.device != text.device:
+        raise ValueError(f"out must be [{text.numel() // 2}, {s}] on {text.device}")
+    if status is not None:
+        _vec(status, text.numel() // 2, "status", 4)
     with _on(text.device):
         rc = _lib.rsa_encrypt_text(_vp(text.data_ptr()), text.numel(), _p(limbs(e, s)), _p(limbs(n, s)), nbits,
                                    _vp(out.data_ptr()), _vp(status.data_ptr() if status is not None else 0),
@@ -201,9 +238,12 @@ def rsa_decrypt_text(cipher, d: int, n: int, nbits: int, status=None, out=None, 
     """Fused decryption + sec. 2 decoding; returns a CUDA uint8 tensor of letters."""
     import torch
     s = nlimbs(nbits)
-    cipher = cipher.contiguous()
+    cipher = _rows(cipher.contiguous(), s, "cipher")
     if out is None:
         out = torch.empty(2 * cipher.shape[0], dtype=torch.uint8, device=cipher.device)
+    _vec(out, 2 * cipher.shape[0], "out", 1)
+    if status is not None:
+        _vec(status, cipher.shape[0], "status", 4)
     with _on(cipher.device):
         rc = _lib.rsa_decrypt_text(_vp(cipher.data_ptr()), cipher.shape[0], _p(limbs(d, s)), _p(limbs(n, s)), nbits,
                                    _vp(out.data_ptr()), _vp(status.data_ptr() if status is not None else 0),
@@ -216,8 +256,10 @@ def rsa_modexp_batch_host(base: np.ndarray, exp: int, n: int, nbits: int, out: n
     """End-to-end from host memory (H2D, kernel, D2H pipelined); synchronous."""
     s = nlimbs(nbits)
     base = np.ascontiguousarray(base, dtype=np.uint32) if isinstance(base, np.ndarray) else base
+    _rows(base, s, "base", cuda=False)
     if out is None:
         out = np.empty_like(base)
+    _rows(out, s, "out", cuda=False, like=base)
     E, N = limbs(exp, s), limbs(n, s)
     bp = base.ctypes.data if isinstance(base, np.ndarray) else base.data_ptr()
     op = out.ctypes.data if isinstance(out, np.ndarray) else out.data_ptr()
@@ -230,9 +272,12 @@ def rsa_modexp_batch_paper(num, key: int, den: int, faithful: bool = True, out=N
     """The paper's Fig 12 kernel on the GPU (prior art): num is a CUDA
     int32/uint32 tensor of single-word packets; returns result tensor."""
     import torch
+    if not num.is_cuda or num.element_size() != 4:
+        raise ValueError("num must be a CUDA tensor of 32-bit packets")
     num = num.contiguous().view(-1)
     if out is None:
         out = torch.empty_like(num)
+    _vec(out, num.numel(), "out", 4)
     if stream is None:
         stream = torch.cuda.current_stream(num.device).cuda_stream
     elif hasattr(stream, "cuda_stream"):
@@ -256,12 +301,15 @@ def rsa_modexp_batch_multi(base, exps, mods, nbits: int, exp_bits: int | None = 
     """out[i] = base[i]^exps[i] mod mods[i] (CUDA [count, s] 32-bit tensors)."""
     import torch
     s = nlimbs(nbits)
-    for t in (base, exps, mods):
-        if t.dim() != 2 or t.shape[1] != s or not t.is_cuda or t.shape != base.shape:
-            raise ValueError(f"base/exps/mods must be CUDA [count, {s}] tensors")
     base, exps, mods = base.contiguous(), exps.contiguous(), mods.contiguous()
+    _rows(base, s, "base")
+    _rows(exps, s, "exps", like=base)
+    _rows(mods, s, "mods", like=base)
     if out is None:
         out = torch.empty_like(base)
+    _rows(out, s, "out", like=base)
+    if status is not None:
+        _vec(status, base.shape[0], "status", 4)
     exp_bits = 32 * s if exp_bits is None else exp_bits
     with _on(base.device):
         rc = _lib.rsa_modexp_batch_multi(_vp(base.data_ptr()), _vp(exps.data_ptr()), _vp(mods.data_ptr()), nbits,
@@ -274,9 +322,10 @@ def rsa_modexp_batch_multi(base, exps, mods, nbits: int, exp_bits: int | None = 
 
 def rsa_miller_rabin_batch(cand, nbits: int, base: int, out=None, stream=None):
     import torch
-    cand = cand.contiguous()
+    cand = _rows(cand.contiguous(), nlimbs(nbits), "cand")
     if out is None:
         out = torch.empty(cand.shape[0], dtype=torch.int32, device=cand.device)
+    _vec(out, cand.shape[0], "out", 4)
     with _on(cand.device):
         rc = _lib.rsa_miller_rabin_batch(_vp(cand.data_ptr()), nbits, cand.shape[0], base, _vp(out.data_ptr()),
                                          _vp(_stream_of(cand, stream)))
@@ -295,7 +344,7 @@ def rsa_prime_candidates(nbits: int, seed: int, first: int, count: int, device="
 
 def rsa_prime_sieve(cand, nbits: int, stream=None):
     import torch
-    cand = cand.contiguous()
+    cand = _rows(cand.contiguous(), nlimbs(nbits), "cand")
     out = torch.empty(cand.shape[0], dtype=torch.int32, device=cand.device)
     with _on(cand.device):
         rc = _lib.rsa_prime_sieve(_vp(cand.data_ptr()), nbits, cand.shape[0], _vp(out.data_ptr()),
@@ -338,6 +387,28 @@ def rsa_multi_plan_info(nbits: int, exp_bits: int, mr: bool = False) -> dict:
 
 def rsa_set_window(w: int) -> None:
     _check(_lib.rsa_set_window(w), "rsa_set_window")
+
+
+def rsa_set_kernel_path(width_class: int, path: int) -> None:
+    """Select the kernel of a width class (A/B measurement; include/rsa_b200.h)."""
+    _check(_lib.rsa_set_kernel_path(width_class, path), "rsa_set_kernel_path")
+
+
+def rsa_get_kernel_path(width_class: int) -> int:
+    rc = _lib.rsa_get_kernel_path(width_class)
+    if rc < 0:
+        _check(rc, "rsa_get_kernel_path")
+    return rc
+
+
+@contextlib.contextmanager
+def kernel_path(width_class: int, path: int):
+    """with kernel_path(64, RSA_PATH_INT): ... -- restores the default after."""
+    rsa_set_kernel_path(width_class, path)
+    try:
+        yield
+    finally:
+        rsa_set_kernel_path(width_class, RSA_PATH_DEFAULT)
 
 
 def rsa_kernel_launches() -> int:

@@ -9,7 +9,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "librsa_b200.so")
 SOURCES = [os.path.join(CSRC, f) for f in ("modexp.cu", "modexp_f64.cu", "modexp_multi.cu", "crt.cu", "rsa_abi.cpp")]
-DEPS = SOURCES + [os.path.join(CSRC, f) for f in ("mont.cuh", "mont_f64.cuh", "mont_pair.cuh", "mont_sqr.cuh", "mont_multi.cuh", "mont_group.cuh", "plan.h", "host_bn.hpp")] + [
+DEPS = SOURCES + [os.path.join(CSRC, f) for f in ("mont.cuh", "mont_f64.cuh", "mont_pair.cuh", "mont_sqr.cuh", "mont_multi.cuh", "mont_group.cuh", "plan.h", "host_bn.hpp", "devcache.h")] + [
     os.path.join(os.path.dirname(HERE), "include", "rsa_b200.h")]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
@@ -22,19 +22,34 @@ def stale() -> bool:
     return any(os.path.getmtime(d) > t for d in DEPS)
 
 
+def _compile_link(out: str, extra: list[str], verbose: bool) -> None:
+    """One nvcc per translation unit, in parallel, then one link (the units
+    are independent; the FP64 and integer kernels dominate the build time)."""
+    objdir = os.path.join(HERE, "build", os.path.basename(out).replace(".", "_"))
+    os.makedirs(objdir, exist_ok=True)
+    procs = []
+    objs = []
+    for src in SOURCES:
+        obj = os.path.join(objdir, os.path.basename(src) + ".o")
+        objs.append(obj)
+        cmd = [NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", *extra,
+               "-Xptxas", "-v" if verbose else "-O3", "-c", "-o", obj, src]
+        procs.append((cmd, subprocess.Popen(cmd)))
+    failed = [cmd for cmd, p in procs if p.wait() != 0]
+    if failed:
+        raise subprocess.CalledProcessError(1, failed[0])
+    subprocess.check_call([NVCC, *ARCH, "-shared", "-o", out, *objs])
+
+
 def build(force: bool = False, verbose: bool = False, out: str | None = None) -> str:
     """Build the library (to `out` for an A/B variant, loaded with RSA_B200_LIB)."""
+    extra = os.environ.get("RSA_B200_NVCC_EXTRA", "").split()   # A/B experiments, e.g. -DRSA_SMALL_PPT2=8
     if out:
-        extra = os.environ.get("RSA_B200_NVCC_EXTRA", "").split()
-        subprocess.check_call([NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-shared", "-Xcompiler", "-fPIC",
-                               *extra, "-o", out, *SOURCES])
+        _compile_link(out, extra, verbose)
         return out
     if not force and not stale():
         return LIB
-    extra = os.environ.get("RSA_B200_NVCC_EXTRA", "").split()   # A/B experiments, e.g. -DRSA_SMALL_PPT2=8
-    cmd = [NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-shared", "-Xcompiler", "-fPIC", *extra,
-           "-Xptxas", "-v" if verbose else "-O3", "-o", LIB + ".tmp", *SOURCES]
-    subprocess.check_call(cmd)
+    _compile_link(LIB + ".tmp", extra, verbose)
     os.replace(LIB + ".tmp", LIB)
     # the microbenchmarks (roofline denominator, chain latency), built alongside
     for name in ("imad_peak", "imad_latency", "dfma_latency"):

@@ -12,6 +12,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include "devcache.h"
 #include "mont.cuh"
 #include "mont_sqr.cuh"
 
@@ -134,12 +135,14 @@ static cudaError_t crt_launch(const void* raw, int which, unsigned long long cou
     const size_t smem = sizeof(uint4) * (SH / 4) * block;
     const unsigned grid = (unsigned)((count + block - 1) / block);
     const CrtParams<SH>& prm = *static_cast<const CrtParams<SH>*>(raw);
-    static bool attr = false;
-    if (!attr) {
-        cudaFuncSetAttribute(crt_split_kernel<SH>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        cudaFuncSetAttribute(crt_combine_kernel<SH>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        attr = true;
-    }
+    static AttrCache cache;
+    cudaError_t e = cached_attr(cache, [&]() {
+        cudaError_t r = cudaFuncSetAttribute(crt_split_kernel<SH>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)smem);
+        if (r != cudaSuccess) return r;
+        return cudaFuncSetAttribute(crt_combine_kernel<SH>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    });
+    if (e != cudaSuccess) return e;
     if (which == 0) crt_split_kernel<SH><<<grid, block, smem, st>>>(prm);
     else crt_combine_kernel<SH><<<grid, block, smem, st>>>(prm);
     return cudaGetLastError();

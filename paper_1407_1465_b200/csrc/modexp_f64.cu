@@ -18,6 +18,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include "devcache.h"
 #include "mont_f64.cuh"
 #include "plan.h"
 
@@ -244,15 +245,11 @@ static cudaError_t launch_f64(const void* params, int sms, cudaStream_t stream, 
                               size_t* slots_out, bool query_only) {
     const int block = F64Cfg<S>::BLOCK;
     const size_t smem = sizeof(double) * F64Cfg<S>::ND * ((F64Cfg<S>::SQR || F64Cfg<S>::ASMEM) && !F64Cfg<S>::ONESLOT ? 2 : 1) * block;
-    static int occ = -1;
-    if (occ < 0) {
-        cudaError_t e = cudaFuncSetAttribute(modexp_f64_kernel<S>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             (int)smem);
-        if (e != cudaSuccess) return e;
-        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, modexp_f64_kernel<S>, block, smem);
-        if (e != cudaSuccess) return e;
-        if (occ < 1) occ = 1;
-    }
+    static OccCache cache;
+    int occ = 0;
+    cudaError_t ce = cached_occupancy(
+        cache, [&](int* o) { return occupancy_with_smem(modexp_f64_kernel<S>, block, smem, o); }, &occ);
+    if (ce != cudaSuccess) return ce;
     int grid = sms * occ;
     if (grid_out) *grid_out = grid;
     if (block_out) *block_out = block;

@@ -19,6 +19,7 @@
 #include <stdint.h>
 #include <type_traits>
 
+#include "devcache.h"
 #include "mont_multi.cuh"
 
 namespace rsa_b200 {
@@ -341,9 +342,28 @@ __global__ void prime_candidates_kernel(uint64_t seed, unsigned long long first,
 
 // verdict[i] = 0 if candidate i has a prime factor < 2^12 (and is not that
 // prime), else 1.  Horner with 64-bit remainders.
-__constant__ uint16_t c_small_primes[564];
-__global__ void sieve_kernel(const uint32_t* __restrict__ cand, unsigned long long count, int s_io, int nprimes,
-                             uint32_t* __restrict__ verdict) {
+struct SmallPrimes {
+    int count;
+    uint16_t p[564];
+};
+// the odd primes < 2^12, computed once on the host (a kernel parameter: no
+// per-device __constant__ upload to keep in sync)
+static const SmallPrimes& small_primes() {
+    static const SmallPrimes sp = [] {
+        SmallPrimes s{};
+        for (uint32_t x = 3; x < 4096 && s.count < 564; x += 2) {
+            bool is = true;
+            for (uint32_t f = 3; f * f <= x; f += 2)
+                if (x % f == 0) { is = false; break; }
+            if (is) s.p[s.count++] = (uint16_t)x;
+        }
+        return s;
+    }();
+    return sp;
+}
+__global__ void sieve_kernel(const uint32_t* __restrict__ cand, unsigned long long count, int s_io,
+                             const __grid_constant__ SmallPrimes sp, uint32_t* __restrict__ verdict) {
+    const int nprimes = sp.count;
     const unsigned long long i = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x;
     if (i >= count) return;
     const uint32_t* c = cand + i * (unsigned long long)s_io;
@@ -351,7 +371,7 @@ __global__ void sieve_kernel(const uint32_t* __restrict__ cand, unsigned long lo
     for (int k = 1; k < s_io; k++) one_limb = one_limb && c[k] == 0;
     uint32_t ok = 1;
     for (int t = 0; t < nprimes && ok; t++) {
-        const uint32_t pr = c_small_primes[t];
+        const uint32_t pr = sp.p[t];
         uint64_t r = 0;
         for (int k = s_io - 1; k >= 0; k--) r = ((r << 32) | c[k]) % pr;
         if (r == 0 && !(one_limb && c[0] == pr)) ok = 0;
@@ -367,15 +387,11 @@ static cudaError_t launch_multi(const MultiParams& prm, int sms, cudaStream_t st
                                 bool query_only) {
     const int block = MCfg<S>::BLOCK;
     const size_t smem = sizeof(uint4) * (S / 2) * block;
-    static int occ = -1;
-    if (occ < 0) {
-        cudaError_t e = cudaFuncSetAttribute(modexp_multi_kernel<S>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             (int)smem);
-        if (e != cudaSuccess) return e;
-        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, modexp_multi_kernel<S>, block, smem);
-        if (e != cudaSuccess) return e;
-        if (occ < 1) occ = 1;
-    }
+    static OccCache cache;
+    int occ = 0;
+    cudaError_t ce = cached_occupancy(
+        cache, [&](int* o) { return occupancy_with_smem(modexp_multi_kernel<S>, block, smem, o); }, &occ);
+    if (ce != cudaSuccess) return ce;
     const int grid = sms * occ;
     if (slots_out) *slots_out = (size_t)grid * block;
     if (query_only) return cudaSuccess;
@@ -423,22 +439,8 @@ cudaError_t rsa_b200_prime_candidates(uint64_t seed, unsigned long long first, u
 
 cudaError_t rsa_b200_sieve(const uint32_t* cand, unsigned long long count, int s_io, uint32_t* verdict,
                            cudaStream_t stream) {
-    static bool init = false;
-    static int np = 0;
-    if (!init) {
-        uint16_t pr[564];
-        for (uint32_t x = 3; x < 4096 && np < 564; x += 2) {
-            bool is = true;
-            for (uint32_t f = 3; f * f <= x; f += 2)
-                if (x % f == 0) { is = false; break; }
-            if (is) pr[np++] = (uint16_t)x;
-        }
-        cudaError_t e = cudaMemcpyToSymbol(rsa_b200::c_small_primes, pr, sizeof(uint16_t) * np);
-        if (e != cudaSuccess) return e;
-        init = true;
-    }
     if (!count) return cudaSuccess;
     const unsigned blocks = (unsigned)((count + 127) / 128);
-    rsa_b200::sieve_kernel<<<blocks, 128, 0, stream>>>(cand, count, s_io, np, verdict);
+    rsa_b200::sieve_kernel<<<blocks, 128, 0, stream>>>(cand, count, s_io, rsa_b200::small_primes(), verdict);
     return cudaGetLastError();
 }

@@ -95,3 +95,46 @@ def test_plan_montmul_counts():
     bits, pop = k["d"].bit_length(), bin(k["d"]).count("1")
     assert pd["montmuls"] < (bits - 1) + (pop - 1) + 2          # beats Fig 5 binary
     assert pd["squarings"] >= bits - 1 - pd["window"]
+
+
+def test_kernel_path_knob():
+    """rsa_set_kernel_path validates (class, path) pairs, resolves per class and
+    changes the plan (executed products) without touching a device."""
+    import paper_1407_1465_b200 as R
+    import workload
+    defaults = {2: R.RSA_PATH_INT_MULTI, 4: R.RSA_PATH_INT_MULTI, 8: R.RSA_PATH_INT, 16: R.RSA_PATH_INT,
+                32: R.RSA_PATH_FP64, 64: R.RSA_PATH_FP64, 128: R.RSA_PATH_FP64}
+    for S, p in defaults.items():
+        assert R.rsa_get_kernel_path(S) == p, S
+    for S, p in [(8, R.RSA_PATH_FP64), (64, R.RSA_PATH_INT_PAIR), (128, R.RSA_PATH_INT_MULTI), (3, 0), (64, 9)]:
+        with pytest.raises(R.RsaError):
+            R.rsa_set_kernel_path(S, p)
+    with pytest.raises(R.RsaError):
+        R.rsa_get_kernel_path(5)
+    k = workload.key("rsa2048")
+    fp = R.rsa_plan_info(k["d"], k["n"], 2048)
+    with R.kernel_path(64, R.RSA_PATH_INT_GROUP):
+        grp = R.rsa_plan_info(k["d"], k["n"], 2048)
+        assert R.rsa_get_kernel_path(64) == R.RSA_PATH_INT_GROUP
+    with R.kernel_path(128, R.RSA_PATH_INT):           # S = 128 integer = the lane pairs
+        assert R.rsa_get_kernel_path(128) == R.RSA_PATH_INT_PAIR
+    assert R.rsa_get_kernel_path(64) == R.RSA_PATH_FP64
+    assert fp["fp64_digits"] == 40 and fp["sqr_kernel"] == 1
+    assert grp["fp64_digits"] == 0 and grp["sqr_kernel"] == 0
+    assert grp["products"] > fp["products"]          # no dedicated squaring on the group kernel
+    assert R.rsa_plan_info(k["d"], k["n"], 2048) == fp
+
+
+def test_binding_rejects_bad_shapes():
+    """The binding checks [count, s] / element size / residency before the C side
+    trusts count*s (host arrays checked without a GPU)."""
+    import numpy as np
+    import paper_1407_1465_b200 as R
+    import workload
+    k = workload.key("rsa2048")
+    # (numpy inputs are converted with ascontiguousarray(uint32): values, not layouts, are accepted)
+    for bad in [np.zeros(64 * 3, np.uint32), np.zeros((3, 63), np.uint32), np.zeros((3, 64, 1), np.uint32)]:
+        with pytest.raises(ValueError):
+            R.rsa_modexp_batch_host(bad, 3, k["n"], 2048)
+    with pytest.raises(ValueError):
+        R.rsa_modexp_batch_host(np.zeros((3, 64), np.uint32), 3, k["n"], 2048, out=np.zeros((2, 64), np.uint32))
