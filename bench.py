@@ -7,8 +7,11 @@ Default workload (BASELINE.json metric "RSA-2048 modexps/sec (e=65537 and full
 d)"): one step = encrypt a 1M-packet batch with e = 65537, then decrypt the
 ciphertexts with the full private exponent d (configs[2] then configs[3]), all
 packets resident in HBM.  value = modexps per second (2 x packets per step),
-whole job.  Under torchrun each rank runs its own full-size batch (weak
-scaling, no collective in the timed region: packets are independent).
+whole job.  Under torchrun (N > 1) the SAME batch is sharded (strong scaling,
+SURVEY.md sec. 8(e)): rank r holds only its contiguous slice
+(paper_1407_1465_b200.shard), runs the legs on it, and the step ends with the
+all-gather of the result slices into the whole result on every rank (row a9);
+time = max over ranks.
 
 Prints ONE JSON line on rank 0.  See DESIGN.md "Measurement" for every field.
 """
@@ -143,23 +146,48 @@ class ClockSampler:
 
 # ------------------------------------------------------------------ oracle baseline
 
+def cpu_model() -> str:
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    import platform
+    return platform.processor() or "unknown"
+
+
 def cpu_baseline(key: dict, base: np.ndarray, legs, cpu_seconds: float):
     """The oracle (oracle/, plain C, as it stands) on the host cores, on a
-    bounded sample of the same workload: the first `k` packets, every leg."""
+    bounded sample of the same workload, every leg (SURVEY.md sec. 8(d)
+    "Oracle timing"): a fixed 4096-packet subsample (the first 4096 packets of
+    the batch, edge packets included) for the expensive full-d legs, more
+    packets for cheap legs (about cpu_seconds of single-core work); all cores
+    (one thread each); plus the single-core rate on a smaller share; the CPU
+    model is named (the paper names its CPU)."""
     import oracle
     cores = os.cpu_count() or 1
     # calibrate on 2 random (non-edge) packets of the most expensive leg
     t0 = time.perf_counter()
     oracle.modexp_batch(base[16:18], key[legs[-1][1]], key["n"], nthreads=1)
     per = max(time.perf_counter() - t0, 1e-6) / 2 * len(legs)
-    k = int(max(cores, min(len(base), cpu_seconds / per)))
-    k = min(k, len(base))
+    k = min(len(base), 4096 if per > 1e-3 else max(4096, int(cpu_seconds / per)))
     t0 = time.perf_counter()
     cur = base[:k]
     for _, field in legs:
         cur = oracle.modexp_batch(cur, key[field], key["n"], nthreads=cores)
     wall = time.perf_counter() - t0
+    k1 = min(k, max(16, k // (2 * cores)))
+    t0 = time.perf_counter()
+    cur = base[:k1]
+    for _, field in legs:
+        cur = oracle.modexp_batch(cur, key[field], key["n"], nthreads=1)
+    wall1 = time.perf_counter() - t0
     return {"value": k * len(legs) / wall, "unit": "modexp/s", "cores": cores, "kind": "oracle",
+            "cpu_model": cpu_model(),
+            "single_core": {"value": k1 * len(legs) / wall1, "unit": "modexp/s",
+                            "sample": f"first {k1} packets, {len(legs)} leg(s), 1 thread, {wall1:.1f} s"},
             "sample": f"first {k} packets of the batch, {len(legs)} leg(s) each "
                       f"({', '.join(l for l, _ in legs)}); {wall:.1f} s wall on {cores} threads"}
 
@@ -199,14 +227,19 @@ def measured_dfma_rate():
 
 
 def measured_digit_mix_rate():
-    """Best FP64 ops/clk/SM of the digit-product instruction mix (DFMA.RZ, DADD,
-    DFMA.RZ + a 64-bit column add) in profiles/r01_dfma_latency.jsonl, or None."""
+    """Best FP64 ops/clk/SM of the kernel's digit-product instruction mix
+    (DFMA.RZ, DADD, DFMA.RZ + the 64-bit column add: the rows with mix
+    'dfma+dadd+dfma+iadd3x2' only, not the add-free or IMAD.X variants) in
+    profiles/r01_dfma_latency.jsonl, or None."""
     best = None
     try:
         with open(os.path.join(ROOT, "profiles", "r01_dfma_latency.jsonl")) as f:
             for line in f:
                 if line.startswith("{"):
-                    v = json.loads(line).get("fp64_ops_per_clk_per_sm")
+                    rec = json.loads(line)
+                    if rec.get("mix") != "dfma+dadd+dfma+iadd3x2":
+                        continue
+                    v = rec.get("fp64_ops_per_clk_per_sm")
                     if v is not None:
                         best = v if best is None or v > best else best
     except (OSError, ValueError):
@@ -214,17 +247,17 @@ def measured_digit_mix_rate():
     return best
 
 
-def batch_kernel_name(S: int, fp64: bool = False) -> str:
-    """The kernel modexp.cu launches for width class S (same env switches)."""
-    if fp64:
+def batch_kernel_name(R, S: int) -> str:
+    """The kernel modexp.cu launches for width class S (its resolved path)."""
+    path = R.rsa_get_kernel_path(S)
+    if path == R.RSA_PATH_FP64:
         return f"modexp_f64_kernel<{S}>"
-    if S <= 4 and os.environ.get("RSA_B200_SMALL", "1")[:1] != "0":
+    if path == R.RSA_PATH_INT_MULTI:
         return f"modexp_small_kernel<{S}>"
-    if S == 64 and os.environ.get("RSA_B200_SHAPE64", "")[:1] == "g":
-        return "modexp_group_kernel<64, 2>"
-    if S == 128:
-        return "modexp_group_kernel<128, 4>" if os.environ.get("RSA_B200_TPI128", "")[:1] == "4" \
-            else "modexp_pair_kernel<128>"
+    if path == R.RSA_PATH_INT_GROUP:
+        return f"modexp_group_kernel<{S}, {2 if S == 64 else 4}>"
+    if path == R.RSA_PATH_INT_PAIR:
+        return f"modexp_pair_kernel<{S}>"
     return f"modexp_kernel<{S}>"
 
 
@@ -270,11 +303,12 @@ def run_reference(args, rank, world):
     value = k * len(legs) / (ms / 1e3)
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "modexp/s", "n_gpus": 1,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "u32", "data": "synthetic",
+            "scaling": "strong", "vs_baseline": None, "dtype": "u32", "data": "synthetic",
             "config": {"workload": args.config, "packets_per_step": k, "key": key_name,
                        "note": "oracle (plain C bignum, Fig 5 L2R) on host cores; bounded sample per step"},
             "cpu_baseline": {"value": value, "unit": "modexp/s", "cores": cores, "kind": "oracle",
-                             "sample": f"{k} packets x {len(legs)} legs per step"},
+                             "cpu_model": cpu_model(),
+                             "sample": f"first {k} packets of the batch x {len(legs)} legs per step"},
             "e2e": {"value": value, "unit": "modexp/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -283,32 +317,44 @@ def run_ours(args, rank, world, local_rank):
     import torch
     import torch.distributed as dist
     import paper_1407_1465_b200 as R
+    from paper_1407_1465_b200.shard import gather_slices, modexp_sharded_host, shard_bounds
 
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
-    key_name, count, legs = WORKLOADS[args.config]
+    key_name, total, legs = WORKLOADS[args.config]
     if args.count:
-        count = args.count
+        total = args.count
     key = workload.key(key_name)
     nb, n = key["nbits"], key["n"]
     s = workload.limbs_needed(nb)
-    # each rank: its own full-size batch (weak scaling); seeds differ per rank
+    # strong scaling: ONE batch of `total` packets (the same on every rank), rank
+    # r holds only rows [lo, hi) on its device
+    bounds, per = shard_bounds(total, world)
+    lo, hi = bounds[rank]
+    count = hi - lo
     kind = legs[0][1].split(":")[0] if ":" in legs[0][1] else "batch"
     stream = torch.cuda.current_stream(dev)
+    base_np = None
     if kind == "text":
-        rng = np.random.default_rng(workload.MASTER_SEED + rank)
-        letters = torch.from_numpy((rng.integers(0, 26, 2 * count) + ord("a")).astype(np.uint8)).to(dev)
+        rng = np.random.default_rng(workload.MASTER_SEED)
+        text_np = (rng.integers(0, 26, 2 * total) + ord("a")).astype(np.uint8)
+        letters = torch.from_numpy(text_np[2 * lo:2 * hi].copy()).to(dev)
         base = letters
-        base_np = None
     elif kind == "mr":
         nb = int(legs[0][1].split(":")[1])
         s = workload.limbs_needed(nb)
-        base = R.rsa_prime_candidates(nb, workload.MASTER_SEED + rank, 0, count, device=dev)
-        base_np = None
+        # counter-based generator: this rank's candidates are indices [lo, hi)
+        base = R.rsa_prime_candidates(nb, workload.MASTER_SEED, lo, count, device=dev)
     else:
-        base_np = workload.packets(count, nb, n=n, config_id=2 + 100 * rank)
-        base = torch.from_numpy(base_np.view(np.int32)).to(dev)
-    bufs = [base] + [torch.empty_like(base) for _ in legs]
+        full_np = workload.packets(total, nb, n=n, config_id=2)
+        base_np = full_np[lo:hi]
+        base = torch.from_numpy(np.ascontiguousarray(base_np).view(np.int32)).to(dev)
+    # the result rows go straight into this rank's chunk of the gather buffer
+    # (shard.py layout): rows [rank*per, rank*per + count) of [per*world, s]
+    gathered = kind in ("batch", "crt", "multi")
+    full = torch.empty((per * world if world > 1 else count, s), dtype=torch.int32, device=dev) if gathered else None
+    mine = full[rank * per:rank * per + count] if (gathered and world > 1) else full
+    bufs = [base] + [torch.empty_like(base) for _ in legs[:-1]] + [mine if gathered else torch.empty_like(base)]
     if kind == "text":
         bufs = [letters, torch.empty((count, s), dtype=torch.int32, device=dev), torch.empty_like(letters)]
         exps = [key["e"], key["d"]]
@@ -318,11 +364,11 @@ def run_ours(args, rank, world, local_rank):
         plans = [R.rsa_plan_info(e, n, nb) for e in exps]
     elif kind == "multi":
         ev = int(legs[0][1].split(":")[1])
-        rng = np.random.Generator(np.random.PCG64(workload.MASTER_SEED + 500 + rank))
-        mods_np = rng.integers(0, 2**32, (count, s), dtype=np.uint64).astype(np.uint32)
+        rng = np.random.Generator(np.random.PCG64(workload.MASTER_SEED + 500))
+        mods_np = rng.integers(0, 2**32, (total, s), dtype=np.uint64).astype(np.uint32)[lo:hi]
         mods_np[:, 0] |= 1
         mods_np[:, s - 1] |= np.uint32(1 << 31)
-        mods = torch.from_numpy(mods_np.view(np.int32)).to(dev)
+        mods = torch.from_numpy(np.ascontiguousarray(mods_np).view(np.int32)).to(dev)
         expt = torch.from_numpy(workload.ints_to_rows([ev] * 1, s).view(np.int32)).to(dev).expand(count, s).contiguous()
         exps = [ev]
         plans = [R.rsa_multi_plan_info(nb, ev.bit_length())]
@@ -340,11 +386,13 @@ def run_ours(args, rank, world, local_rank):
         plans = [R.rsa_multi_plan_info(nb, 0, mr=True)]
         mr_out = torch.empty(count, dtype=torch.int32, device=dev)
 
-    def step(evs=None):
+    def step(evs=None, gev=None):
         for j, e in enumerate(exps):
             if evs is not None:
                 evs[j][0].record(stream)
-            if kind == "batch":
+            if count == 0:
+                pass
+            elif kind == "batch":
                 R.rsa_modexp_batch(bufs[j], e, n, nb, out=bufs[j + 1], stream=stream)
             elif kind == "multi":
                 R.rsa_modexp_batch_multi(bufs[j], expt, mods, nb, exp_bits=e.bit_length(), out=bufs[j + 1],
@@ -359,12 +407,23 @@ def run_ours(args, rank, world, local_rank):
                 R.rsa_miller_rabin_batch(bufs[j], nb, 2, out=mr_out, stream=stream)
             if evs is not None:
                 evs[j][1].record(stream)
+        if gathered and world > 1:
+            # step a9: reassemble the whole result on every rank (in-place all-gather)
+            gather_slices(full, per)
+            if gev is not None:
+                gev.record(stream)
 
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
-    # correctness of the last warm-up round trip (GPU-side compare, cheap)
-    verified = bool(torch.equal(bufs[-1], bufs[0])) if len(legs) == 2 else None
+    # correctness of the last warm-up round trip: the whole reassembled batch
+    # equals the input batch (compared on the host: each rank holds only its
+    # input slice on the device)
+    verified = None
+    if len(legs) == 2 and kind == "batch":
+        verified = bool(np.array_equal(full[:total].cpu().numpy().view(np.uint32), full_np))
+    elif len(legs) == 2:
+        verified = bool(torch.equal(bufs[-1], bufs[0]))
 
     clocks = ClockSampler(local_rank if "CUDA_VISIBLE_DEVICES" not in os.environ else 0)
     if rank == 0:
@@ -372,6 +431,7 @@ def run_ours(args, rank, world, local_rank):
         time.sleep(0.3)
     leg_events = [[[torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)] for _ in legs]
                   for _ in range(args.steps)]
+    gather_events = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     t_start, t_end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     launches0 = R.rsa_kernel_launches()
     if world > 1:
@@ -379,7 +439,7 @@ def run_ours(args, rank, world, local_rank):
     torch.cuda.synchronize()
     t_start.record(stream)
     for k in range(args.steps):
-        step(leg_events[k])
+        step(leg_events[k], gather_events[k])
     t_end.record(stream)
     torch.cuda.synchronize()
     if world > 1:
@@ -389,38 +449,57 @@ def run_ours(args, rank, world, local_rank):
     elapsed_ms = t_start.elapsed_time(t_end)
     leg_ms = [statistics.mean(leg_events[k][j][0].elapsed_time(leg_events[k][j][1]) for k in range(args.steps))
               for j in range(len(legs))]
+    gather_ms = (statistics.mean(leg_events[k][-1][1].elapsed_time(gather_events[k]) for k in range(args.steps))
+                 if gathered and world > 1 else 0.0)
     if world > 1:
         on_dev = dist.get_backend() == "nccl"
-        t = torch.tensor([elapsed_ms] + leg_ms, device=dev if on_dev else "cpu", dtype=torch.float64)
+        t = torch.tensor([elapsed_ms, gather_ms] + leg_ms, device=dev if on_dev else "cpu", dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        elapsed_ms, leg_ms = float(t[0]), [float(v) for v in t[1:]]
+        elapsed_ms, gather_ms, leg_ms = float(t[0]), float(t[1]), [float(v) for v in t[2:]]
+        lt = torch.tensor([launches], device=dev if on_dev else "cpu", dtype=torch.int64)
+        dist.all_reduce(lt, op=dist.ReduceOp.SUM)
+        launches = int(lt[0])
 
-    # ---- end to end through the public host API (pinned host buffers)
+    # ---- end to end through the public API (pinned host buffers): every rank
+    # copies its slice host -> device, runs the legs, the slices are
+    # all-gathered, rank 0 copies the whole result device -> host
     e2e = None
-    if not args.no_e2e and rank == 0 and kind == "batch":
-        host_in = torch.from_numpy(base_np.view(np.int32)).pin_memory()
-        host_mid = [torch.empty_like(host_in).pin_memory() for _ in legs]
-        R.rsa_modexp_batch_host(host_in, exps[0], n, nb, out=host_mid[0])      # warm
+    if not args.no_e2e and kind == "batch":
+        host_in = torch.from_numpy(np.ascontiguousarray(base_np).view(np.int32)).pin_memory()
+        host_out = torch.empty((total, s), dtype=torch.int32).pin_memory() if rank == 0 else None
+        modexp_sharded_host(host_in, exps[:1], n, nb, total, out=host_out)      # warm
         ts = []
         for _ in range(max(1, min(args.steps, 3))):
+            if world > 1:
+                dist.barrier()
             t0 = time.perf_counter()
-            cur = host_in
-            for j, e in enumerate(exps):
-                R.rsa_modexp_batch_host(cur, e, n, nb, out=host_mid[j])
-                cur = host_mid[j]
-            ts.append(time.perf_counter() - t0)
+            modexp_sharded_host(host_in, exps, n, nb, total, out=host_out)
+            torch.cuda.synchronize()
+            dt = time.perf_counter() - t0
+            if world > 1:
+                tt = torch.tensor([dt], dtype=torch.float64,
+                                  device=dev if dist.get_backend() == "nccl" else "cpu")
+                dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+                dt = float(tt[0])
+            ts.append(dt)
         e2e_s = statistics.median(ts)
-        nbytes = count * s * 4 * len(legs)
-        e2e = {"value": count * len(legs) / e2e_s, "unit": "modexp/s", "h2d_bytes_per_step": nbytes,
-               "d2h_bytes_per_step": nbytes, "ms_per_step": 1e3 * e2e_s,
-               "path": "rsa_modexp_batch_host per leg: pinned host -> device -> kernel -> host, chunk-pipelined"}
-        if len(legs) == 2:
-            e2e["verified"] = bool(torch.equal(host_mid[-1], host_in))
+        row = s * 4
+        if world == 1:
+            nh2d = nd2h = total * row * len(legs)
+            path = "rsa_modexp_batch_host per leg: pinned host -> device -> kernel -> host, chunk-pipelined"
+        else:
+            nh2d, nd2h = total * row, total * row
+            path = ("shard.modexp_sharded_host: each rank pinned slice -> its device, legs, NCCL all-gather of the "
+                    "result slices, rank 0 whole result -> pinned host")
+        e2e = {"value": total * len(legs) / e2e_s, "unit": "modexp/s", "h2d_bytes_per_step": nh2d,
+               "d2h_bytes_per_step": nd2h, "ms_per_step": 1e3 * e2e_s, "path": path}
+        if len(legs) == 2 and rank == 0:
+            e2e["verified"] = bool(np.array_equal(host_out.numpy().view(np.uint32), full_np))
 
     if rank != 0:
         return
     ms_per_step = elapsed_ms / args.steps
-    value = world * count * len(legs) / (ms_per_step / 1e3)
+    value = total * len(legs) / (ms_per_step / 1e3)
     # ---- roofline of the dominant kernel
     props = torch.cuda.get_device_properties(dev)
     sms = props.multi_processor_count
@@ -441,9 +520,9 @@ def run_ours(args, rank, world, local_rank):
                 "traffic": ncu_traffic(key_name, legs[dom][0], count),
                 "traffic_unit": "bytes per launch", "algorithmic_bytes": count * s * 4 * 2,
                 "kernel": ({"multi": f"modexp_multi_kernel<{S}>", "mr": f"modexp_multi_kernel<{S}> (MR mode)",
-                            "crt": f"2 x {batch_kernel_name(S, fp64)} + crt_split/combine (half-width CRT legs; "
+                            "crt": f"2 x {batch_kernel_name(R, S)} + crt_split/combine (half-width CRT legs; "
                                    f"products of both)"}.get(
-                    kind, batch_kernel_name(S, fp64))) + f" ({legs[dom][0]})",
+                    kind, batch_kernel_name(R, S))) + f" ({legs[dom][0]})",
                 "algorithmic": f"{plans[dom]['products']} 32x32->64 limb products/packet "
                                f"({plans[dom]['squarings']} squarings x "
                                f"{'1.5S^2+1.5S' if plans[dom]['sqr_kernel'] else '2S^2+S'} + "
@@ -501,7 +580,7 @@ def run_ours(args, rank, world, local_rank):
         roofline["frac_at_measured_clock"] = roofline["frac"] * f_max / clk["sm_mhz"]
     legs_out = {}
     for j, (label, field) in enumerate(legs):
-        legs_out[label] = {"ms": leg_ms[j], "modexp_per_s": world * count / (leg_ms[j] / 1e3),
+        legs_out[label] = {"ms": leg_ms[j], "modexp_per_s": total / (leg_ms[j] / 1e3),
                            "montmuls_per_packet": plans[j]["montmuls"], "squarings_per_packet": plans[j]["squarings"],
                            "products_per_packet": plans[j]["products"], "window": plans[j]["window"],
                            "exp_bits": plans[j]["exp_bits"]}
@@ -509,14 +588,17 @@ def run_ours(args, rank, world, local_rank):
     if not args.no_cpu_baseline and world == 1 and kind == "batch":
         cpu = cpu_baseline(key, base_np, legs, args.cpu_seconds)
     line = {"metric": METRIC, "value": value, "unit": "modexp/s", "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
+            "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f64" if fp64 else "u32", "data": "synthetic",
-            "config": {"workload": args.config, "packets_per_rank": count, "key": key_name + " (seeded, "
+            "config": {"workload": args.config, "packets_total": total, "packets_per_rank": per,
+                       "key": key_name + " (seeded, "
                        "workload/keys.json)", "legs": [l for l, _ in legs], "modulus_bits": nb,
                        "l2": f"inputs {count * s * 4 / 2**20:.0f} MiB per leg vs 126 MB L2"
                              + (" (larger than L2)" if count * s * 4 > 126e6 else " (fits L2)"),
-                       "parallelism": f"dp{world} (independent shards, no collective in the timed region)"},
-            "legs": legs_out, "verified_roundtrip": verified, "roofline": roofline, "cpu_baseline": cpu,
+                       "parallelism": (f"dp{world}: contiguous slices of one {total}-packet batch, one per rank; "
+                                       f"the step ends with the all-gather of the result slices (row a9)"
+                                       if world > 1 else "dp1 (one GPU, the whole batch)")},
+            "legs": legs_out, **({"gather_ms": gather_ms} if world > 1 and gathered else {}), "verified_roundtrip": verified, "roofline": roofline, "cpu_baseline": cpu,
             "e2e": e2e, "gpu_launches": int(launches), "clocks": clk}
     print(json.dumps(line), flush=True)
 

@@ -1,6 +1,8 @@
-"""Multi-process (world_size 2 and 3, gloo, CPU) tests of the batch sharder:
-contiguous slices, padding, all-gather reassembly.  The per-slice compute is
-the oracle here (test infrastructure); on GPUs it is the CUDA path."""
+"""Multi-process (world_size 2..4, gloo, CPU) tests of the batch sharder:
+each rank holds only its contiguous slice; in-place all-gather into the padded
+buffer; round-trip pipelines; empty slices (count < world) and an empty batch.
+The per-slice compute is the oracle here (test infrastructure); on the GPU
+(tests/test_gpu_shard.py) it is the CUDA path."""
 import os
 import socket
 
@@ -42,26 +44,35 @@ def _worker(rank, world, port, count, q):
     try:
         import oracle
         import workload
-        from paper_1407_1465_b200.shard import modexp_sharded
+        from paper_1407_1465_b200.shard import modexp_sharded, modexp_sharded_host
         k = workload.key("rsa256")
         base = workload.packets(count, 256, n=k["n"], config_id=9)
-        full = torch.from_numpy(base.view(np.int32))
-
-        def compute(x):
-            return torch.from_numpy(oracle.modexp_batch(x.numpy().view(np.uint32), k["e"], k["n"]).view(np.int32))
-
-        out = modexp_sharded(full, k["e"], k["n"], 256, compute=compute)
         lo, hi = shard_range(count, rank, world)
-        mine = modexp_sharded(full, k["e"], k["n"], 256, compute=compute, gather=False)
+        local = torch.from_numpy(base[lo:hi].view(np.int32))      # this rank's slice only
+
+        def compute(x, e, o):
+            o.copy_(torch.from_numpy(oracle.modexp_batch(x.numpy().view(np.uint32), e, k["n"]).view(np.int32)))
+            return o
+
+        out = modexp_sharded(local, k["e"], k["n"], 256, count, compute=compute)
+        mine = modexp_sharded(local, k["e"], k["n"], 256, count, compute=compute, gather=False)
+        both = modexp_sharded(local, (k["e"], k["d"]), k["n"], 256, count, compute=compute)
         want = oracle.modexp_batch(base, k["e"], k["n"])
-        ok = np.array_equal(out.numpy().view(np.uint32), want) and \
-            np.array_equal(mine.numpy().view(np.uint32), want[lo:hi])
+        ok = out.shape[0] == count and np.array_equal(out.numpy().view(np.uint32), want) and \
+            np.array_equal(mine.numpy().view(np.uint32), want[lo:hi]) and \
+            np.array_equal(both.numpy().view(np.uint32), base)
+        # a wrong slice is rejected before any compute
+        try:
+            modexp_sharded(torch.zeros((hi - lo + 1, 8), dtype=torch.int32), 3, k["n"], 256, count, compute=compute)
+            ok = False
+        except ValueError:
+            pass
         q.put((rank, ok))
     finally:
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world,count", [(2, 1001), (3, 10), (2, 1)])
+@pytest.mark.parametrize("world,count", [(2, 1001), (3, 10), (2, 1), (4, 3), (3, 0)])
 def test_gloo_all_gather_reassembly(world, count):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
