@@ -88,9 +88,9 @@ int rsa_validate_key(const uint32_t* e, const uint32_t* d, const uint32_t* p,
  *               workspace allocation) and returns; completion is observed
  *               through the stream.  count == 0 is a no-op returning RSA_OK.
  * Kernels (results identical; chosen by measurement): moduli of
- * 513..4096 bits run on the FP64 pipe (52-bit digits, exact DFMA.RZ products);
- * narrower ones, and these too with the environment variables RSA_B200_F64=0
- * (513..2048 bits) or RSA_B200_F64_4096=0 (2049..4096), on the integer (IMAD) pipe.
+ * 513..4096 bits run on the FP64 pipe (52-bit digits, exact DFMA.RZ products),
+ * narrower ones on the integer (IMAD) pipe; rsa_set_kernel_path (below)
+ * selects the alternates per width class for A/B measurement.
  * Errors: RSA_EINVAL, RSA_ERANGE, RSA_EEVEN, RSA_ECUDA. */
 int rsa_modexp_batch(const uint32_t* base, const uint32_t* exp, const uint32_t* n,
                      int nbits, size_t count, uint32_t* out, void* stream);
@@ -128,6 +128,31 @@ int rsa_decrypt_crt_batch(const uint32_t* c, const uint32_t* p, const uint32_t* 
  * Errors: RSA_ERANGE (den or key out of range), RSA_EINVAL, RSA_ECUDA. */
 int rsa_modexp_batch_paper(const uint32_t* num, uint64_t key, uint32_t den, size_t count,
                            uint32_t* result, int faithful, void* stream);
+
+/* The paper's exponentiation schedules as selectable single-word GPU kernels
+ * (SURVEY.md sec. 8(f) row f2), one thread per packet, 64-bit exact products
+ * (den < 2^32), for replaying the paper's toy keys on B200 beside the
+ * Montgomery path:
+ *   RSA_SCHED_NAIVE            Fig 4: c = g mod m, then
+ *                              exp - 1 times c = c g mod m (O(exp));
+ *   RSA_SCHED_R2L              Fig 5a: right-to-left binary;
+ *   RSA_SCHED_L2R              Fig 5b: left-to-right binary;
+ *   RSA_SCHED_HALVING          Fig 12, exact, exp = 0 -> 1;
+ *   RSA_SCHED_HALVING_FAITHFUL Fig 12 with its exp = 0 -> g mod m (reading Z5).
+ *   num, out : DEVICE pointers, `count` uint32 values each (out may be num);
+ *   1 <= den < 2^32 (Fig 12: < 2^31); exp < 2^32 for NAIVE and the Fig 12
+ *   schedules (their loops are O(exp)), any 64-bit exp for R2L / L2R.
+ * Every schedule returns num^exp mod den (0^0 = 1 mod den), except the
+ * faithful Fig 12 at exp = 0.  Asynchronous on `stream`.
+ * Errors: RSA_ERANGE (den or exp out of range), RSA_EINVAL (null pointer,
+ * unknown schedule), RSA_ECUDA. */
+#define RSA_SCHED_NAIVE             1
+#define RSA_SCHED_R2L               2
+#define RSA_SCHED_L2R               3
+#define RSA_SCHED_HALVING           4
+#define RSA_SCHED_HALVING_FAITHFUL  5
+int rsa_modexp_batch_schedule(const uint32_t* num, uint64_t exp, uint32_t den, size_t count, uint32_t* out,
+                              int schedule, void* stream);
 
 /* ---- multi-key batches and GPU prime search ----
  * rsa_modexp_batch_multi: out[i] = base[i]^exps[i] mod mods[i], every packet

@@ -37,8 +37,10 @@ EXPORTS = ["rsa_strerror", "rsa_keygen_check", "rsa_validate_key", "rsa_modexp_b
            "rsa_kernel_launches", "rsa_modexp_batch_paper", "rsa_modexp_batch_multi", "rsa_miller_rabin_batch",
            "rsa_prime_candidates", "rsa_prime_sieve", "rsa_prime_search", "rsa_keygen", "rsa_multi_plan_info",
            "rsa_decrypt_crt_batch", "rsa_encrypt_text", "rsa_decrypt_text", "rsa_set_kernel_path",
-           "rsa_get_kernel_path"]
+           "rsa_get_kernel_path", "rsa_modexp_batch_schedule"]
 # kernel paths per width class (rsa_set_kernel_path; include/rsa_b200.h)
+# the paper's single-word schedules (rsa_modexp_batch_schedule)
+RSA_SCHED_NAIVE, RSA_SCHED_R2L, RSA_SCHED_L2R, RSA_SCHED_HALVING, RSA_SCHED_HALVING_FAITHFUL = 1, 2, 3, 4, 5
 RSA_PATH_DEFAULT, RSA_PATH_FP64, RSA_PATH_INT, RSA_PATH_INT_GROUP, RSA_PATH_INT_PAIR, RSA_PATH_INT_MULTI = range(6)
 
 if not os.path.exists(LIB_PATH):
@@ -67,6 +69,8 @@ _lib.rsa_modexp_batch_host.argtypes = [ctypes.c_void_p, _u32p, _u32p, ctypes.c_i
                                        ctypes.c_void_p]
 _lib.rsa_plan_info.argtypes = [_u32p, _u32p, ctypes.c_int, ctypes.POINTER(RsaPlanInfo)]
 _lib.rsa_set_window.argtypes = [ctypes.c_int]
+_lib.rsa_modexp_batch_schedule.argtypes = [ctypes.c_void_p, ctypes.c_uint64, ctypes.c_uint32, ctypes.c_size_t,
+                                           ctypes.c_void_p, ctypes.c_int, ctypes.c_void_p]
 _lib.rsa_set_kernel_path.argtypes = [ctypes.c_int, ctypes.c_int]
 _lib.rsa_get_kernel_path.argtypes = [ctypes.c_int]
 _lib.rsa_encode.argtypes = [ctypes.c_char_p, _u32p, ctypes.c_size_t, ctypes.POINTER(ctypes.c_size_t)]
@@ -286,6 +290,25 @@ def rsa_modexp_batch_paper(num, key: int, den: int, faithful: bool = True, out=N
         rc = _lib.rsa_modexp_batch_paper(ctypes.c_void_p(num.data_ptr()), key, den, num.numel(),
                                          ctypes.c_void_p(out.data_ptr()), 1 if faithful else 0, ctypes.c_void_p(stream))
     _check(rc, "rsa_modexp_batch_paper")
+    return out
+
+
+def rsa_modexp_batch_schedule(num, exp: int, den: int, schedule: int, out=None, stream=None):
+    """num^exp mod den by one of the paper's schedules (Fig 4 naive, Fig 5a
+    right-to-left, Fig 5b left-to-right, Fig 12 halving) on the GPU: num is a
+    CUDA tensor of 32-bit single-word packets; returns the result tensor."""
+    import torch
+    if not num.is_cuda or num.element_size() != 4:
+        raise ValueError("num must be a CUDA tensor of 32-bit packets")
+    num = num.contiguous().view(-1)
+    if out is None:
+        out = torch.empty_like(num)
+    _vec(out, num.numel(), "out", 4)
+    with _on(num.device):
+        rc = _lib.rsa_modexp_batch_schedule(ctypes.c_void_p(num.data_ptr()), exp, den, num.numel(),
+                                            ctypes.c_void_p(out.data_ptr()), schedule,
+                                            ctypes.c_void_p(_stream_of(num, stream)))
+    _check(rc, "rsa_modexp_batch_schedule")
     return out
 
 

@@ -504,6 +504,52 @@ __global__ void paper_fig12_kernel(const uint32_t* __restrict__ num, uint64_t ke
 }
 
 
+// The paper's other single-word schedules, one
+// thread per packet, exact 64-bit products (den < 2^32): Fig 4 naive repeated
+// multiplication, Fig 5a right-to-left and Fig 5b
+// left-to-right binary square-and-multiply, each step as
+// printed ("(u * v) mod m", Fig 3, as a 64-bit remainder).
+enum ToySched { TOY_NAIVE = 1, TOY_R2L = 2, TOY_L2R = 3 };
+
+template <int SCHED>
+__global__ void paper_schedule_kernel(const uint32_t* __restrict__ num, uint64_t e, uint32_t den,
+                                      unsigned long long count, uint32_t* __restrict__ out) {
+    const unsigned long long i = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x;
+    if (i >= count) return;
+    const uint64_t m = den, g = num[i];
+    uint64_t A;
+    if constexpr (SCHED == TOY_NAIVE) {
+        // c_1 = g mod m; c_j = c_{j-1} g mod m, j = 2 .. e (e - 1 multiplications)
+        if (e == 0) {
+            A = 1 % m;
+        } else {
+            const uint64_t gm = g % m;
+            A = gm;
+            for (uint64_t j = 2; j <= e; j++) A = (A * gm) % m;
+        }
+    } else if constexpr (SCHED == TOY_R2L) {
+        // 1. A = 1, S = g, E = e.  2. while E != 0: 2.1 E odd -> A = A S mod m,
+        // E = E - 1; 2.2 E = E / 2; 2.3 E != 0 -> S = S S mod m.  3. return A
+        uint64_t S = g, E = e;
+        A = 1;
+        while (E != 0) {
+            if (E & 1) { A = (A * S) % m; E -= 1; }
+            E >>= 1;
+            if (E != 0) S = (S * S) % m;
+        }
+        A %= m;
+    } else {
+        // 1. A = 1.  2. for i = t .. 0: 2.1 A = A A mod m; 2.2 e_i = 1 -> A = A g mod m
+        const uint64_t gm = g % m;
+        A = 1 % m;
+        for (int b = 63 - (e ? __clzll((long long)e) : 63); e && b >= 0; b--) {
+            A = (A * A) % m;
+            if ((e >> b) & 1) A = (A * gm) % m;
+        }
+    }
+    out[i] = (uint32_t)A;
+}
+
 // ---------------------------------------------------------------------------
 // S = TPI * L limbs with TPI lanes per packet (mont_group.cuh): the 4096-bit
 // class runs TPI = 4 (L = 32, ~2x the resident warps of the lane-pair shape).
@@ -841,6 +887,21 @@ cudaError_t rsa_b200_codec(const void* params, int io, int path, int sms, cudaSt
 cudaError_t rsa_b200_fill_one(uint32_t* out, unsigned long long count, int s_io, int sms, cudaStream_t stream) {
     if (count == 0) return cudaSuccess;
     rsa_b200::fill_one_kernel<<<sms * 4, 256, 0, stream>>>(out, count, s_io);
+    return cudaGetLastError();
+}
+
+cudaError_t rsa_b200_paper_schedule(const uint32_t* num, uint64_t e, uint32_t den, unsigned long long count,
+                                    int sched, uint32_t* out, cudaStream_t stream) {
+    if (count == 0) return cudaSuccess;
+    const int block = 64;   // the paper's Table 1 shape, as for Fig 12
+    const unsigned grid = (unsigned)((count + block - 1) / block);
+    using namespace rsa_b200;
+    switch (sched) {
+    case TOY_NAIVE: paper_schedule_kernel<TOY_NAIVE><<<grid, block, 0, stream>>>(num, e, den, count, out); break;
+    case TOY_R2L: paper_schedule_kernel<TOY_R2L><<<grid, block, 0, stream>>>(num, e, den, count, out); break;
+    case TOY_L2R: paper_schedule_kernel<TOY_L2R><<<grid, block, 0, stream>>>(num, e, den, count, out); break;
+    default: return cudaErrorInvalidValue;
+    }
     return cudaGetLastError();
 }
 

@@ -47,6 +47,8 @@ void rsa_b200_crt_fill(int SH, void* raw, const uint32_t* c, uint32_t* cp, uint3
 cudaError_t rsa_b200_crt_launch(int SH, const void* raw, int which, unsigned long long count, cudaStream_t st);
 cudaError_t rsa_b200_paper_fig12(const uint32_t* num, uint64_t key, uint32_t den, unsigned long long count,
                                  int faithful, uint32_t* result, cudaStream_t stream);
+cudaError_t rsa_b200_paper_schedule(const uint32_t* num, uint64_t e, uint32_t den, unsigned long long count,
+                                    int sched, uint32_t* out, cudaStream_t stream);
 
 using rsa_host::BN;
 
@@ -675,6 +677,21 @@ int rsa_modexp_batch_paper(const uint32_t* num, uint64_t key, uint32_t den, size
     return RSA_OK;
 }
 
+int rsa_modexp_batch_schedule(const uint32_t* num, uint64_t exp, uint32_t den, size_t count, uint32_t* out,
+                              int schedule, void* stream) {
+    if (schedule == RSA_SCHED_HALVING || schedule == RSA_SCHED_HALVING_FAITHFUL)
+        return rsa_modexp_batch_paper(num, exp, den, count, out, schedule == RSA_SCHED_HALVING_FAITHFUL, stream);
+    if (schedule != RSA_SCHED_NAIVE && schedule != RSA_SCHED_R2L && schedule != RSA_SCHED_L2R) return RSA_EINVAL;
+    if (den == 0) return RSA_ERANGE;
+    if (schedule == RSA_SCHED_NAIVE && exp >= (1ull << 32)) return RSA_ERANGE;
+    if (count == 0) return RSA_OK;
+    if (!num || !out) return RSA_EINVAL;
+    // RSA_SCHED_* 1..3 are the kernel's TOY_NAIVE / TOY_R2L / TOY_L2R
+    if (rsa_b200_paper_schedule(num, exp, den, count, schedule, out, (cudaStream_t)stream) != cudaSuccess)
+        return RSA_ECUDA;
+    g_launches++;
+    return RSA_OK;
+}
 
 int rsa_multi_plan_info(int nbits, int exp_bits, int mr, rsa_plan_info_t* info) {
     if (!info) return RSA_EINVAL;

@@ -1,12 +1,14 @@
 #!/usr/bin/env python3
 """Replay the paper's Table 1 / Table 2 shapes on B200 (SURVEY.md sec. 8(f)
 row f2): the paper's own Fig 12 kernel (rsa_modexp_batch_paper, 64 threads
-per block, O(e) loop) beside the Montgomery path (rsa_modexp_batch), same
+per block, O(e) loop), its other schedules as GPU kernels (Fig 4 naive, Fig 5a
+right-to-left, Fig 5b left-to-right: rsa_modexp_batch_schedule) beside the
+Montgomery path (rsa_modexp_batch), same
 inputs (values 0..800), device time by CUDA events (median of
 20 runs, the paper averaged 20).  Context only: the paper's
 seconds were GT 630M wall clock including transfers.
 
-    python tests/tools/paper_tables.py > profiles/r01_paper_tables.json
+    python tests/tools/paper_tables.py > profiles/r02_paper_tables.json
 """
 import json
 import os
@@ -54,9 +56,17 @@ def main():
             want = oracle.modexp_batch(pp[:k], e, n).ravel()
             ok = bool(np.array_equal(o1.cpu().numpy().view(np.uint32)[:k], want) and
                       np.array_equal(o2.cpu().numpy().view(np.uint32).ravel()[:k], want))
-            out["rows"].append({"table": name, "cite": cite, "size": size, "paper_fig12_ms": ms_paper,
-                                "montgomery_ms": ms_mont, "paper_fig12_modexp_per_s": size / ms_paper * 1e3,
-                                "montgomery_modexp_per_s": size / ms_mont * 1e3, "oracle_checked": ok})
+            row = {"table": name, "cite": cite, "size": size, "paper_fig12_ms": ms_paper,
+                   "montgomery_ms": ms_mont, "paper_fig12_modexp_per_s": size / ms_paper * 1e3,
+                   "montgomery_modexp_per_s": size / ms_mont * 1e3}
+            for label, sched in (("naive_fig4", R.RSA_SCHED_NAIVE), ("r2l_fig5a", R.RSA_SCHED_R2L),
+                                 ("l2r_fig5b", R.RSA_SCHED_L2R)):
+                o3 = torch.empty_like(t1)
+                row[label + "_ms"] = timed(lambda: R.rsa_modexp_batch_schedule(t1, e, n, sched, out=o3))
+                row[label + "_modexp_per_s"] = size / row[label + "_ms"] * 1e3
+                ok = ok and bool(np.array_equal(o3.cpu().numpy().view(np.uint32)[:k], want))
+            row["oracle_checked"] = ok
+            out["rows"].append(row)
     print(json.dumps(out, indent=1))
 
 
