@@ -824,8 +824,9 @@ int rsa_b200_resolve_path(int S) {
 // multiply: the multi-packet, group and pair kernels and the 4096-bit FP64
 // kernel have no squaring path.  Used for the window choice and the
 // executed-product count of rsa_plan_info.
+int rsa_b200_f64_sqr(int S);
 int rsa_b200_sqr_dedicated(int S, int path) {
-    if (path == RSA_PATH_FP64) return S < 128 ? 1 : 0;
+    if (path == RSA_PATH_FP64) return rsa_b200_f64_sqr(S);
     return (path == RSA_PATH_INT && S <= 64) ? 1 : 0;
 }
 

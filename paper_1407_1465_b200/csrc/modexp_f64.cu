@@ -48,6 +48,12 @@ namespace rsa_b200 {
 #ifndef RSA_F64_MINB32
 #define RSA_F64_MINB32 4
 #endif
+#ifndef RSA_F64_SQR128
+#define RSA_F64_SQR128 1    // 4096-bit kernel: dedicated squaring with A in its one slot (montsqr_slot)
+#endif
+#ifndef RSA_F64_BLOCK128
+#define RSA_F64_BLOCK128 256   // 4096-bit kernel CTA: 256 threads in lockstep (the unrolled squaring is long)
+#endif
 template <int S>
 struct F64Cfg {
     static constexpr int ND = rsa_f64_digits(S);
@@ -56,19 +62,22 @@ struct F64Cfg {
     // of SASS, and drifting warps stall on instruction fetch (ncu:
     // no_instruction).  S = 32 (ND = 20): ~80 registers of state, small code,
     // several independent CTAs per SM.
-    static constexpr int BLOCK = (S == 64) ? RSA_F64_BLOCK : 128;
-    static constexpr int MINB = (S == 64) ? (RSA_F64_BLOCK >= 256 ? 1 : 256 / RSA_F64_BLOCK)
-                                          : (S == 32 ? RSA_F64_MINB32 : RSA_F64_MINB128);
+    static constexpr int BLOCK = (S == 64) ? RSA_F64_BLOCK : (S == 128 ? RSA_F64_BLOCK128 : 128);
+    static constexpr int MINB = (S == 64)    ? (RSA_F64_BLOCK >= 256 ? 1 : 256 / RSA_F64_BLOCK)
+                                : (S == 128) ? (RSA_F64_BLOCK128 >= 256 ? 1 : RSA_F64_MINB128)
+                                             : RSA_F64_MINB32;
 #ifndef RSA_F64_LOCK
 #define RSA_F64_LOCK 0      // A/B: lockstep barriers with 2 x 128-thread CTAs (557K vs 589K)
 #endif
-    static constexpr bool LOCKSTEP = (S == 64) && (RSA_F64_BLOCK >= 256 || RSA_F64_LOCK);
+    static constexpr bool LOCKSTEP = ((S == 64) && (RSA_F64_BLOCK >= 256 || RSA_F64_LOCK)) ||
+                                     ((S == 128) && RSA_F64_BLOCK128 >= 256);
     // S = 128 (ND = 80): the square's 2 ND digits and A + B slots do not fit shared memory at
     // 8 warps/SM, so every op is the CIOS multiply with A parked in a single ND-digit slot and B
     // read in place (the slot itself for squarings, the window table in global memory, or a
     // per-block constant): ND^2 products more per squaring, no squaring code.
     static constexpr bool ONESLOT = (S >= 128);
     static constexpr bool SQR = RSA_F64_SQR && !ONESLOT;   // dedicated squaring (montsqr) vs montmul(a, a)
+    static constexpr bool SQRSLOT = ONESLOT && RSA_F64_SQR128;   // ONESLOT squarings by montsqr_slot
     static constexpr bool ASMEM = ONESLOT || ((S >= 64) && RSA_F64_ASMEM && SQR);   // montmul's A parked in smem
 };
 
@@ -97,6 +106,16 @@ modexp_f64_kernel(const __grid_constant__ ModexpF64Params<S> p) {
         }
     }
     __syncthreads();
+    // RSA_F64_NCONST: n's digits are read from the parameter block (constant
+    // bank); 2^104 then lives in an ordinary (non-uniform) register so the
+    // DFMA's one constant-bank operand slot is left to the digit of n
+    const double* const nsrc = RSA_F64_NCONST ? p.nd : nds;
+    double c104 = p.c104;
+    if constexpr (RSA_F64_NCONST != 0) {
+        unsigned z;
+        asm volatile("mov.u32 %0, %%laneid;\n\tand.b32 %0, %0, 0;" : "=r"(z));
+        c104 = __longlong_as_double(__double_as_longlong(c104) + z);
+    }
 
     // every thread runs the same number of trips (uniform barriers); an
     // out-of-range trip recomputes the last packet and skips the store
@@ -161,17 +180,25 @@ modexp_f64_kernel(const __grid_constant__ ModexpF64Params<S> p) {
                 } else if (op.kind == RSA_OP_R2) { bp = cst; P = 2; Q = 1; }
                 else { bp = cst + ND; P = 2; Q = 1; }   // RSA_OP_ONE (plans for this class carry no MULX)
                 auto bget = [&](int i) -> double { return bp[(size_t)(i >> 1) * P + (i & 1) * Q]; };
-                if (RSA_F64_SQRSMEM && op.kind == RSA_OP_SQR) {
+                if (F64Cfg<S>::SQRSLOT && op.kind == RSA_OP_SQR) {
+                    // dedicated squaring: ND (ND+1)/2 + ND^2 digit products, A stays in the slot
+                    for (int r = 0; r < op.rep; r++) {
+                        if constexpr (F64Cfg<S>::LOCKSTEP) __syncthreads();
+                        f64::montsqr_slot<ND>(nsrc, p.np52, c104, t, bsm, stride);
+                    }
+                } else if (RSA_F64_SQRSMEM && op.kind == RSA_OP_SQR) {
                     // squarings (the bulk): b is the slot itself, read with explicit
                     // shared-memory loads instead of generic ones
                     auto bsq = [&](int i) -> double { return f64::ld_digit(bsm + (size_t)i * stride); };
                     for (int r = 0; r < op.rep; r++)
-                        f64::montmul<ND, true, decltype(bsq), true, RSA_F64_FUSEJ>(a, bsq, nds, p.np52, p.c104, t,
+                        f64::montmul<ND, true, decltype(bsq), true, RSA_F64_FUSEJ>(a, bsq, nsrc, p.np52, c104, t,
                                                                                   bsm, stride);
                 } else {
-                    for (int r = 0; r < op.rep; r++)
-                        f64::montmul<ND, true, decltype(bget), true, RSA_F64_FUSEJ>(a, bget, nds, p.np52, p.c104, t,
+                    for (int r = 0; r < op.rep; r++) {
+                        if constexpr (F64Cfg<S>::LOCKSTEP) __syncthreads();
+                        f64::montmul<ND, true, decltype(bget), true, RSA_F64_FUSEJ>(a, bget, nsrc, p.np52, c104, t,
                                                                                    bsm, stride);
+                    }
                 }
             } else
             for (int r = 0; r < op.rep; r++) {
@@ -181,7 +208,7 @@ modexp_f64_kernel(const __grid_constant__ ModexpF64Params<S> p) {
                 if (op.kind == RSA_OP_SQR) {
                     if constexpr (F64Cfg<S>::SQR) {
                         // the square's 2 ND digits go to this thread's slot
-                        f64::montsqr<ND>(a, nds, p.np52, p.c104, t, reinterpret_cast<uint64_t*>(bsm), stride);
+                        f64::montsqr<ND>(a, nsrc, p.np52, c104, t, reinterpret_cast<uint64_t*>(bsm), stride);
                         continue;
                     } else {
 #pragma unroll
@@ -208,7 +235,7 @@ modexp_f64_kernel(const __grid_constant__ ModexpF64Params<S> p) {
                 }
                 // b occupies digits [0, ND) of the slot; A is parked in [ND, 2 ND)
                 f64::montmul<ND, F64Cfg<S>::ASMEM, decltype(from_smem), false, RSA_F64_FUSEJ64 != 0>(
-                    a, from_smem, nds, p.np52, p.c104, t, bsm + ND * stride, stride);
+                    a, from_smem, nsrc, p.np52, c104, t, bsm + ND * stride, stride);
             }
             if (op.flags & RSA_F_STORE) {
 #pragma unroll
@@ -265,6 +292,18 @@ static cudaError_t launch_f64(const void* params, int sms, cudaStream_t stream, 
 }  // namespace rsa_b200
 
 // host entry points (C++ linkage) used by modexp.cu's dispatch
+
+// 1 if the FP64 kernel of class S squares with a dedicated squaring
+// (ND (ND+1)/2 + ND^2 digit products), 0 if with the CIOS multiply (2 ND^2)
+int rsa_b200_f64_sqr(int S) {
+    using namespace rsa_b200;
+    switch (S) {
+    case 32: return F64Cfg<32>::SQR ? 1 : 0;
+    case 64: return F64Cfg<64>::SQR ? 1 : 0;
+    case 128: return F64Cfg<128>::SQRSLOT ? 1 : 0;
+    default: return 0;
+    }
+}
 cudaError_t rsa_b200_launch_f64(int S, const void* params, int sms, cudaStream_t stream, int* grid, int* block,
                                 size_t* slots, bool query_only) {
     using namespace rsa_b200;

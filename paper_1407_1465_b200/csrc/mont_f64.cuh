@@ -58,6 +58,18 @@
 #ifndef RSA_F64_NREG
 #define RSA_F64_NREG 0   // A/B: n in registers in the reduction loop, 552K vs 591K at 2048 (CRT-2048 even)
 #endif
+#ifndef RSA_F64_NCONST
+#define RSA_F64_NCONST 0  // n's digits as constant-bank DFMA operands (kernel parameters) instead of smem pairs
+#endif
+#ifndef RSA_F64_SQBATCH
+#define RSA_F64_SQBATCH 4  // recursive product scan: digit products issued per batch (even; A/B at
+#endif                     // 4096: 2/4/8/12 -> 62.5K/63.5K/63.4K/63.0K)
+#ifndef RSA_F64_SQACC2
+#define RSA_F64_SQACC2 0   // recursive product scan: two partial sums per column sum (A/B)
+#endif
+#ifndef RSA_F64_SQLOOP
+#define RSA_F64_SQLOOP 40  // product scan as plain unrolled loops up to this ND (ptxas stops unrolling
+#endif                     // the loop form at ND = 80: the recursive form expands at compile time)
 #ifndef RSA_F64_MU
 #define RSA_F64_MU 1      // CIOS loop trips unrolled (A/B: 2 -> 561K vs 565K at 2048, 37.4K vs 60.2K at 4096)
 #endif
@@ -118,8 +130,16 @@ __host__ __device__ __forceinline__ double sub_rn(double a, double b) {   // exa
 // and the load is volatile: ptxas may neither hoist the ND digits into
 // registers ahead of the loop (which starves the product schedule) nor fold
 // them into uniform registers (too few: they spill).
+// RSA_F64_NCONST: nd points to the kernel-parameter copy instead; the loads
+// are plain, so ptxas can take each digit as a constant-bank operand of the
+// DFMAs (no load instruction, no register read).
 __host__ __device__ __forceinline__ void nd_pair(const double* nd, int g, double& x, double& y) {
 #ifdef __CUDA_ARCH__
+    if constexpr (RSA_F64_NCONST != 0) {
+        x = nd[2 * g];
+        y = nd[2 * g + 1];
+        return;
+    }
     asm volatile("ld.volatile.shared.v2.f64 {%0, %1}, [%2];"
                  : "=d"(x), "=d"(y) : "r"((unsigned)__cvta_generic_to_shared(nd + 2 * g)));
 #else
@@ -334,6 +354,206 @@ __host__ __device__ __forceinline__ void montmul(double (&a)[ND], BF b, const do
     }
 }
 
+// Squaring, separated operand scanning (SOS), in three pieces shared by
+// montsqr (registers + a 2 ND-digit slot) and montsqr_slot (one ND-digit slot):
+//
+// number of cross products a_i a_j (i < j, i + j = k, j < ND) in column k
+template <int ND>
+__host__ __device__ constexpr int sqr_ncross(int k) {
+    const int lo = k - ND + 1 > 0 ? k - ND + 1 : 0, hi = (k - 1) / 2;
+    return (k >= 1 && hi >= lo) ? hi - lo + 1 : 0;
+}
+
+// One column K of the product scan, then (recursively, fully expanded at
+// compile time) the columns after it.  xh = the previous column's cross
+// products' high halves, already summed (raw patterns): each product's high
+// half goes straight into the next column's running sum instead of being held
+// until then (at ND = 80 the ~40 pending highs would take 80 registers next to
+// A's 160 and starve the product schedule); lows and highs are added two
+// products at a time (3-input 64-bit adds).
+template <int ND, int K, typename Put>
+__host__ __device__ __forceinline__ void sqr_col(const double (&a)[ND], uint64_t xh, uint64_t hd, uint64_t carry,
+                                                 Put& put) {
+    if constexpr (K < 2 * ND) {
+        constexpr int ILO = K - ND + 1 > 0 ? K - ND + 1 : 0;
+        constexpr int NH = sqr_ncross<ND>(K), NHP = (K >= 1) ? sqr_ncross<ND>(K - 1) : 0;
+        uint64_t x = xh, xn = 0, x2 = 0, xn2 = 0;
+        // products in batches of SQB (every h, then every s = C2 - h, then every
+        // l): the batch is the number of exact splits in flight per warp
+        constexpr int SQB = RSA_F64_SQBATCH;
+#pragma unroll
+        for (int m0 = 0; m0 < NH; m0 += SQB) {
+            double hb[SQB], lb[SQB];
+#pragma unroll
+            for (int u = 0; u < SQB; u++)
+                if (m0 + u < NH) hb[u] = fma_rz(a[ILO + m0 + u], a[K - ILO - m0 - u], C104);
+#pragma unroll
+            for (int u = 0; u < SQB; u++)
+                if (m0 + u < NH) lb[u] = sub_rn(C2, hb[u]);
+#pragma unroll
+            for (int u = 0; u < SQB; u++)
+                if (m0 + u < NH) lb[u] = fma_rz(a[ILO + m0 + u], a[K - ILO - m0 - u], lb[u]);
+#pragma unroll
+            for (int u = 0; u < SQB; u += 2) {
+                // RSA_F64_SQACC2: alternate pairs go to second partial sums
+                uint64_t& xs = (RSA_F64_SQACC2 && ((m0 + u) / 2) % 2) ? x2 : x;
+                uint64_t& xns = (RSA_F64_SQACC2 && ((m0 + u) / 2) % 2) ? xn2 : xn;
+                if (m0 + u + 1 < NH) {
+                    xs += bits(lb[u]) + bits(lb[u + 1]);
+                    xns += bits(hb[u]) + bits(hb[u + 1]);
+                } else if (m0 + u < NH) {
+                    xs += bits(lb[u]);
+                    xns += bits(hb[u]);
+                }
+            }
+        }
+        x += x2;
+        xn += xn2;
+        // exponent fields: BL per low half, BH per high half carried in
+        constexpr uint64_t XB = (uint64_t)NH * BL + (uint64_t)NHP * BH;
+        uint64_t y = hd;
+        constexpr uint64_t YB0 = ((K - 1) >= 0 && ((K - 1) & 1) == 0 && (K - 1) / 2 < ND) ? BH : 0;
+        uint64_t yb = YB0, hdn = 0;
+        if constexpr ((K & 1) == 0 && K / 2 < ND) {
+            const double ai = a[K / 2];
+            const double h = fma_rz(ai, ai, C104);
+            const double l = fma_rz(ai, ai, sub_rn(C2, h));
+            y += bits(l);
+            yb += BL;
+            hdn = bits(h);
+        }
+        const uint64_t v = 2 * (x - XB) + (y - yb) + carry;
+        put(K, v & M52);
+        sqr_col<ND, K + 1>(a, xn, hdn, v >> D, put);
+    }
+}
+
+// sqr_scan: T = A^2 by product scanning, fully unrolled: column k sums the
+// low halves of its cross products a_i a_j (i < j, i + j = k) and the high
+// halves of column k-1's, once; the column is then doubled and the diagonal
+// a_{k/2}^2 added (one 64-bit shift-add per column, not per product).  Column
+// k's digit (< 2^52) is handed to put(k, v) as soon as it completes.
+template <int ND, typename Put>
+__host__ __device__ __forceinline__ void sqr_scan(const double (&a)[ND], Put put) {
+    if constexpr (ND <= RSA_F64_SQLOOP) {
+        uint64_t carry = 0;
+        uint64_t hx[ND], hd = 0;          // high halves pending for the next column (cross, diagonal)
+        int nhx = 0;
+#pragma unroll
+        for (int k = 0; k < 2 * ND; k++) {
+            uint64_t x = 0, xb = 0;       // cross sum (raw patterns) and its exponent fields
+#pragma unroll
+            for (int m = 0; m < ND; m++)
+                if (m < nhx) { x += hx[m]; xb += BH; }
+            int nh = 0;
+#pragma unroll
+            for (int i = 0; i < ND; i++) {
+                const int j = k - i;
+                if (i < j && j < ND) {
+                    const double h = fma_rz(a[i], a[j], C104);
+                    const double l = fma_rz(a[i], a[j], sub_rn(C2, h));
+                    x += bits(l);
+                    xb += BL;
+                    hx[nh++] = bits(h);
+                }
+            }
+            nhx = nh;
+            uint64_t y = hd, yb = (k > 0 && ((k - 1) & 1) == 0 && (k - 1) / 2 < ND) ? BH : 0;
+            hd = 0;
+            if ((k & 1) == 0 && k / 2 < ND) {
+                const double ai = a[k / 2];
+                const double h = fma_rz(ai, ai, C104);
+                const double l = fma_rz(ai, ai, sub_rn(C2, h));
+                y += bits(l);
+                yb += BL;
+                hd = bits(h);
+            }
+            const uint64_t v = 2 * (x - xb) + (y - yb) + carry;
+            carry = v >> D;
+            put(k, v & M52);
+        }
+    } else {
+        sqr_col<ND, 0>(a, 0, 0, 0, put);
+    }
+}
+
+// sqr_reduce: Montgomery reduction of T_low (in t): ND reduction-only CIOS
+// iterations q = t_0 n' mod 2^52; t = (t + q n) / 2^52.  Software-pipelined:
+// the new column 0 is complete once the j = 1 product is in, so the next
+// quotient digit (an IMAD/LOP/DADD chain) is computed there and overlaps the
+// remaining ND-2 products.  Leaves column p carrying BH + (ND-1-p)(BL+BH).
+template <int ND, int RU>
+__host__ __device__ __forceinline__ void sqr_reduce(uint64_t (&t)[ND], const double* __restrict__ nd, uint64_t np,
+                                                    double c104) {
+    uint64_t bias0 = BL;
+    double qd = digit_to_double(((t[0] & M52) * np) & M52);
+    // RSA_F64_NREG: n's digits held in registers for the loop (A's registers are
+    // free here) instead of ND/2 shared-memory pair loads per iteration (A/B)
+    [[maybe_unused]] double nr[RSA_F64_NREG ? ND : 2];
+    if constexpr (RSA_F64_NREG != 0) {
+#pragma unroll
+        for (int g = 0; g < ND / 2; g++) nd_pair(nd, g, nr[2 * g], nr[2 * g + 1]);
+    }
+    auto npair = [&](int g, double& x, double& y) {
+        if constexpr (RSA_F64_NREG != 0) { x = nr[2 * g]; y = nr[2 * g + 1]; }
+        else nd_pair(nd, g, x, y);
+    };
+#ifdef __CUDA_ARCH__
+#pragma unroll RU
+#endif
+    for (int i = 0; i < ND; i++) {
+        double n0, n1;
+        npair(0, n0, n1);
+        const double hq0 = fma_rz(qd, n0, c104);
+        const double lq0 = fma_rz(qd, n0, sub_rn(C2, hq0));
+        const uint64_t cr = (t[0] + bits(lq0) - bias0) >> D;   // column 0 is 0 mod 2^52
+        const double hq1 = fma_rz(qd, n1, c104);
+        const double lq1 = fma_rz(qd, n1, sub_rn(C2, hq1));
+        t[0] = t[1] + bits(lq1) + bits(hq0) + cr;
+        const double qnext = digit_to_double(((t[0] & M52) * np) & M52);
+        uint64_t hqp = bits(hq1);
+#pragma unroll
+        for (int j = 2; j < ND; j++) {
+            double nj = n1;
+            if ((j & 1) == 0) npair(j / 2, nj, n1);
+            const double h = fma_rz(qd, nj, c104);
+            const double l = fma_rz(qd, nj, sub_rn(C2, h));
+            t[j - 1] = t[j] + bits(l) + hqp;
+            hqp = bits(h);
+        }
+        t[ND - 1] = hqp;
+        qd = qnext;
+        bias0 += BL + BH;
+    }
+}
+
+// sqr_finish: t + T_high (high(p) = digit p of T_high), bias removed and
+// carries normalised; out(p, digit) receives the result digits (< 2n in all:
+// T / R + Q n / R < 4n^2/R + n < 2n).
+template <int ND, typename High, typename Out>
+__host__ __device__ __forceinline__ void sqr_finish(uint64_t (&t)[ND], High high, Out out) {
+    if constexpr ((ND >= 64) ? RSA_F64_LOOKAHEAD_BIG : (ND <= 20 ? RSA_F64_LOOKAHEAD_SMALL : RSA_F64_LOOKAHEAD)) {
+#pragma unroll
+        for (int p = 0; p < ND; p++) t[p] = t[p] - (BH + (uint64_t)(ND - 1 - p) * (BL + BH)) + high(p);
+        normalize<ND>(t);
+#pragma unroll
+        for (int p = 0; p < ND; p++) out(p, t[p]);
+    } else {
+        uint64_t carry = 0;
+#pragma unroll
+        for (int p = 0; p < ND; p++) {
+            const uint64_t v = t[p] - (BH + (uint64_t)(ND - 1 - p) * (BL + BH)) + high(p) + carry;
+            t[p] = v & M52;
+            carry = v >> D;
+            out(p, t[p]);
+        }
+    }
+}
+
+// (montsqr keeps its own inline copy of the scan / reduction / finish rather
+// than calling sqr_scan / sqr_reduce / sqr_finish below: with the shared
+// pieces ptxas schedules the 2048-bit squaring ~7% slower, 552K vs 591K
+// decrypts/s, measured.)
 // A <- A^2 R^-1 (mod n), result < 2n for A < 2n (squarings are ~85% of a
 // full-d exponentiation).  A square has ND (ND+1)/2 distinct digit products
 // instead of ND^2, so this is separated operand scanning (SOS):
@@ -351,41 +571,45 @@ template <int ND, int RU = (ND >= 40 ? kRU : kRUs)>
 __host__ __device__ __forceinline__ void montsqr(double (&a)[ND], const double* __restrict__ nd, uint64_t np,
                                                  double c104, uint64_t (&t)[ND], uint64_t* th, int stride) {
     // 1. T = A^2
-    uint64_t carry = 0;
-    uint64_t hx[ND], hd = 0;          // high halves pending for the next column (cross, diagonal)
-    int nhx = 0;
+    if constexpr (ND > RSA_F64_SQLOOP) {
+        sqr_scan<ND>(a, [&](int kk, uint64_t v) { th[kk * stride] = v; });
+    } else {
+        uint64_t carry = 0;
+        uint64_t hx[ND], hd = 0;          // high halves pending for the next column (cross, diagonal)
+        int nhx = 0;
 #pragma unroll
-    for (int k = 0; k < 2 * ND; k++) {
-        uint64_t x = 0, xb = 0;       // cross sum (raw patterns) and its exponent fields
+        for (int k = 0; k < 2 * ND; k++) {
+            uint64_t x = 0, xb = 0;       // cross sum (raw patterns) and its exponent fields
 #pragma unroll
-        for (int m = 0; m < ND; m++)
-            if (m < nhx) { x += hx[m]; xb += BH; }
-        int nh = 0;
+            for (int m = 0; m < ND; m++)
+                if (m < nhx) { x += hx[m]; xb += BH; }
+            int nh = 0;
 #pragma unroll
-        for (int i = 0; i < ND; i++) {
-            const int j = k - i;
-            if (i < j && j < ND) {
-                const double h = fma_rz(a[i], a[j], C104);
-                const double l = fma_rz(a[i], a[j], sub_rn(C2, h));
-                x += bits(l);
-                xb += BL;
-                hx[nh++] = bits(h);
+            for (int i = 0; i < ND; i++) {
+                const int j = k - i;
+                if (i < j && j < ND) {
+                    const double h = fma_rz(a[i], a[j], C104);
+                    const double l = fma_rz(a[i], a[j], sub_rn(C2, h));
+                    x += bits(l);
+                    xb += BL;
+                    hx[nh++] = bits(h);
+                }
             }
+            nhx = nh;
+            uint64_t y = hd, yb = (k > 0 && ((k - 1) & 1) == 0 && (k - 1) / 2 < ND) ? BH : 0;
+            hd = 0;
+            if ((k & 1) == 0 && k / 2 < ND) {
+                const double ai = a[k / 2];
+                const double h = fma_rz(ai, ai, C104);
+                const double l = fma_rz(ai, ai, sub_rn(C2, h));
+                y += bits(l);
+                yb += BL;
+                hd = bits(h);
+            }
+            const uint64_t v = 2 * (x - xb) + (y - yb) + carry;
+            carry = v >> D;
+            th[k * stride] = v & M52;
         }
-        nhx = nh;
-        uint64_t y = hd, yb = (k > 0 && ((k - 1) & 1) == 0 && (k - 1) / 2 < ND) ? BH : 0;
-        hd = 0;
-        if ((k & 1) == 0 && k / 2 < ND) {
-            const double ai = a[k / 2];
-            const double h = fma_rz(ai, ai, C104);
-            const double l = fma_rz(ai, ai, sub_rn(C2, h));
-            y += bits(l);
-            yb += BL;
-            hd = bits(h);
-        }
-        const uint64_t v = 2 * (x - xb) + (y - yb) + carry;
-        carry = v >> D;
-        th[k * stride] = v & M52;
     }
 #pragma unroll
     for (int p = 0; p < ND; p++) t[p] = th[p * stride];
@@ -440,7 +664,7 @@ __host__ __device__ __forceinline__ void montsqr(double (&a)[ND], const double* 
 #pragma unroll
         for (int p = 0; p < ND; p++) a[p] = digit_to_double(t[p]);
     } else {
-        carry = 0;
+        uint64_t carry = 0;
 #pragma unroll
         for (int p = 0; p < ND; p++) {
             const uint64_t v = t[p] - (BH + (uint64_t)(ND - 1 - p) * (BL + BH)) + th[(ND + p) * stride] + carry;
@@ -449,6 +673,39 @@ __host__ __device__ __forceinline__ void montsqr(double (&a)[ND], const double* 
             a[p] = digit_to_double(t[p]);
         }
     }
+}
+
+// The same squaring with A living in this thread's ND-digit shared-memory
+// slot aslot[k * stride] (the 4096-bit kernel, where a second slot does not
+// fit): A is read into registers, T_low goes to the slot as its columns
+// complete, T_high stays in registers: column k uses a_i only for
+// i >= k - ND + 1, so once column k >= ND is done a_0 .. a_{k-ND+1} are dead
+// and T_high digit k - ND takes one of their registers (the live count stays
+// ~2 ND registers).  T_low and T_high then swap places
+// (t <- slot, slot <- T_high), the reduction runs on t, and the result goes
+// back to the slot.  ND (ND+1)/2 + ND^2 digit products instead of the
+// multiply's 2 ND^2.  The slot is accessed through one type (64-bit patterns)
+// only, so no load or store in here can be reordered across another.
+template <int ND, int RU = (ND >= 40 ? kRU : kRUs)>
+__host__ __device__ __forceinline__ void montsqr_slot(const double* __restrict__ nd, uint64_t np, double c104,
+                                                      uint64_t (&t)[ND], double* aslot, int stride) {
+    uint64_t* const s64 = reinterpret_cast<uint64_t*>(aslot);
+    double a[ND];
+#pragma unroll
+    for (int k = 0; k < ND; k++) a[k] = from_bits(s64[k * stride]);
+    uint64_t th[ND];
+    sqr_scan<ND>(a, [&](int k, uint64_t v) {
+        if (k < ND) s64[k * stride] = v;
+        else th[k - ND] = v;
+    });
+#pragma unroll
+    for (int p = 0; p < ND; p++) {
+        t[p] = s64[p * stride];
+        s64[p * stride] = th[p];
+    }
+    sqr_reduce<ND, RU>(t, nd, np, c104);
+    sqr_finish<ND>(t, [&](int p) { return s64[p * stride]; },
+                   [&](int p, uint64_t d) { s64[p * stride] = bits(digit_to_double(d)); });
 }
 
 // r <- r - n if r >= n (digits, r < 2n); nu: n's digits as integers

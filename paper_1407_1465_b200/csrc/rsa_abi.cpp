@@ -654,7 +654,7 @@ int rsa_plan_info(const uint32_t* exp, const uint32_t* n, int nbits, rsa_plan_in
     if (pl.path == RSA_PATH_FP64) {
         const long long nd = rsa_f64_digits(pl.S);
         info->fp64_digits = (int)nd;
-        const long long sqd = (pl.S < 128) ? nd * (nd + 1) / 2 + nd * nd : 2 * nd * nd;   // S = 128: no montsqr
+        const long long sqd = info->sqr_kernel ? nd * (nd + 1) / 2 + nd * nd : 2 * nd * nd;
         info->digit_products = pl.squarings * sqd + (pl.montmuls - pl.squarings) * 2 * nd * nd;
     }
     const int sms = device_sms();

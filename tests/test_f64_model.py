@@ -97,8 +97,12 @@ def test_limb_digit_round_trip(model, S):
         assert int(model(f"L {S} {x:x}"), 16) == x
 
 
-@pytest.mark.parametrize("S", [8, 16, 32, 64])
-def test_montsqr_f64_matches_definition(model, S):
+@pytest.mark.parametrize("S,op", [(8, "S"), (16, "S"), (32, "S"), (64, "S"), (8, "Q"), (32, "Q"), (64, "Q"),
+                                  (128, "Q")])
+def test_montsqr_f64_matches_definition(model, S, op):
+    """montsqr (A in registers, T in a 2 ND slot) and montsqr_slot (A living in
+    one ND-digit slot, T_high parked in A's dead registers: the 4096-bit
+    kernel's squaring) against a^2 R^-1 mod n."""
     rng = random.Random(2024 + S)
     ND = nd_of(S)
     R = 1 << (52 * ND)
@@ -106,7 +110,7 @@ def test_montsqr_f64_matches_definition(model, S):
         nbits = 32 * S if trial % 3 else rng.randint(32 * S // 2 + 1, 32 * S)
         n = rand_modulus(rng, S, nbits)
         a = [2 * n - 1, 0, 1, n - 1, n][trial] if trial < 5 else rng.randrange(2 * n)
-        out = model(f"S {S} {n:x} {a:x} {a:x}")
+        out = model(f"{op} {S} {n:x} {a:x} {a:x}")
         assert out != "MISMATCH"
         r = int(out, 16)
         assert r < 2 * n, "almost-Montgomery bound r < 2n"

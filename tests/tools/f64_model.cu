@@ -5,6 +5,7 @@
 //
 // stdin lines:  "M <S> <n> <a> <b>"  -> montmul(a, b) digits, printed as hex
 //               "S <S> <n> <a> <a>"  -> montsqr(a) (the second a is ignored)
+//               "Q <S> <n> <a> <a>"  -> montsqr_slot(a): A in a strided slot
 //               "C <S> <n> <r>"      -> canonicalise(r)
 //               "L <S> <x>"          -> limbs -> digits -> limbs round trip
 // numbers in hex; n' and the digit split are computed here.
@@ -60,7 +61,7 @@ static void run(char op, char** tok) {
     for (int it = 0; it < 7; it++) inv *= 2 - nu[0] * inv;
     const uint64_t np = (0 - inv) & M52;
     uint64_t r[ND];
-    if (op == 'M' || op == 'S' || op == 'A' || op == 'I' || op == 'F') {
+    if (op == 'M' || op == 'S' || op == 'Q' || op == 'A' || op == 'I' || op == 'F') {
         // a, b may be up to 2n: given as digits-of-hex over ND*52 bits
         constexpr int SW = (52 * ND + 31) / 32;
         auto av = parse_hex(tok[1], SW), bv = parse_hex(tok[2], SW);
@@ -80,6 +81,11 @@ static void run(char op, char** tok) {
         if (op == 'S') {
             uint64_t th[2 * ND];
             montsqr<ND>(ad, nd, np, C104, r, th, 1);
+        } else if (op == 'Q') {           // squaring with A living in one strided slot (4096-bit kernel)
+            double slot[3 * ND];
+            for (int k = 0; k < ND; k++) slot[1 + 3 * k] = ad[k];
+            montsqr_slot<ND>(nd, np, C104, r, slot + 1, 3);
+            for (int k = 0; k < ND; k++) ad[k] = slot[1 + 3 * k];
         } else {
             if (op == 'A') {              // the ASMEM variant (A parked in a strided slot)
                 double slot[3 * ND];
