@@ -48,6 +48,9 @@ def main():
     pp = workload.paper_packets(count)
     got = host(R.rsa_modexp_batch_paper(dev(pp.ravel()), 131, 17947))
     assert np.array_equal(got, oracle.modexp_batch(pp, 131, 17947).ravel())
+    for sched in (R.RSA_SCHED_NAIVE, R.RSA_SCHED_R2L, R.RSA_SCHED_L2R):   # the paper's other schedules
+        got = host(R.rsa_modexp_batch_schedule(dev(pp.ravel()), 131, 17947, sched))
+        assert np.array_equal(got, oracle.modexp_batch(pp, 131, 17947).ravel()), sched
     # multi-key + MR + prime search helpers
     rng = np.random.default_rng(0)
     mods = rng.integers(0, 2**32, (count, 8), dtype=np.uint64).astype(np.uint32)
