@@ -530,7 +530,8 @@ def run_ours(args, rank, world, local_rank):
                                f" x {count} packets per launch",
                 "peak_basis": f"{R_PRODUCTS_PER_CLK_PER_SM} products/clk/SM (IMAD.WIDE half rate, "
                               f"profiles/r01_imad_peak.jsonl) x {sms} SMs x {f_max:.0f} MHz "
-                              f"(MEASURED_PEAKS sm_max_mhz)"}
+                              f"(MEASURED_PEAKS sm_max_mhz)",
+                "peak_source": "nominal: MEASURED_PEAKS.json has no INT32 entry; frac is 'of nominal'"}
     if fp64:
         # The dominant kernel runs on the FP64 pipe (mont_f64.cuh): its own
         # roofline is FP64 ops against the measured DFMA issue rate.  The
@@ -551,12 +552,15 @@ def run_ours(args, rank, world, local_rank):
             "peak_basis": f"{DFMA_PER_CLK_PER_SM} FP64 ops/clk/SM (16 FP64 lanes per SM sub-partition: the "
                           f"peak of ncu's sm__inst_executed_pipe_fp64) x {sms} SMs x {f_max:.0f} MHz "
                           f"(MEASURED_PEAKS sm_max_mhz)",
+            "peak_source": "nominal: MEASURED_PEAKS.json has no FP64 entry (hbm_gbs and bf16 only); frac is "
+                           "'of nominal'. peak_measured_* below are this repo's microbenchmarks",
             **({"peak_measured_dfma": dfma * sms * f_max * 1e6 / 1e12,
                 "frac_of_measured_dfma": f_ach / (dfma * sms * f_max * 1e6 / 1e12)} if dfma else {}),
             **({"peak_measured_digit_mix": mix * sms * f_max * 1e6 / 1e12,
                 "frac_of_measured_digit_mix": f_ach / (mix * sms * f_max * 1e6 / 1e12)}
                if (mix := measured_digit_mix_rate()) else {}),
             "imad_equiv": {"achieved": achieved, "peak": peak, "unit": "Tprod/s", "frac": achieved / peak,
+                           "peak_source": "nominal (half-rate IMAD.WIDE, profiles/r01_imad_peak.jsonl)",
                            "basis": "the path's 32x32->64 limb-product count (the metric's '% of IMAD peak') "
                                     "against 32 products/clk/SM on the integer pipe"}})
     if kind == "batch":
