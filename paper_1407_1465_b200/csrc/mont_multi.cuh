@@ -192,6 +192,13 @@ __device__ __forceinline__ void finish_sm(uint32_t (&a)[S], uint32_t (&X)[S], ui
     for (int k = 0; k < S; k++) a[k] = (X[k] & keep) | (a[k] & ~keep);
 }
 
+#ifndef RSA_MULTI_RED
+#define RSA_MULTI_RED 16   // montsqr_sm reduction steps per loop trip (A/B, multi-key RSA-2048 encrypt: 4/8/16 -> 22.0M/22.8M/23.2M; with 16 ptxas keeps the rotated registers off the IMAD pipe)
+#endif
+#ifndef RSA_MULTI_MUL
+#define RSA_MULTI_MUL 8    // montmul_sm CIOS steps per loop trip (multiple of 4)
+#endif
+
 // A <- A * B R^-1 mod n (B in this thread's smem slot, group g at bslot[g*stride])
 template <int S, class NShared>
 __device__ __forceinline__ void montmul_sm(uint32_t (&a)[S], const uint4* __restrict__ bslot, int /*stride*/,
@@ -201,9 +208,9 @@ __device__ __forceinline__ void montmul_sm(uint32_t (&a)[S], const uint4* __rest
 #pragma unroll
     for (int k = 0; k < S; k++) { X[k] = 0; Y[k] = 0; }
 #pragma unroll 1
-    for (int g0 = 0; g0 < S / 4; g0 += 2) {
+    for (int g0 = 0; g0 < S / 4; g0 += RSA_MULTI_MUL / 4) {
 #pragma unroll
-        for (int g = g0; g < g0 + 2; g++) {
+        for (int g = g0; g < g0 + RSA_MULTI_MUL / 4; g++) {
             const uint4 bv = bslot[g * stride];
             cios_step_sm<S, NShared>(X, Y, hi, a, bv.x, n, n0inv);
             cios_step_sm<S, NShared>(Y, X, hi, a, bv.y, n, n0inv);
@@ -222,16 +229,14 @@ __device__ __forceinline__ void montsqr_sm(uint32_t (&a)[S], const NShared& n, u
     uint32_t X[S], Y[S], hi = 0;
 #pragma unroll
     for (int k = 0; k < S; k++) { X[k] = T[k]; Y[k] = 0; }
+    // RSA_MULTI_RED: reduction steps per loop trip (A/B)
 #pragma unroll 1
-    for (int i = 0; i < S; i += 8) {
-        red_step_sm<S, NShared>(X, Y, hi, n, n0inv);
-        red_step_sm<S, NShared>(Y, X, hi, n, n0inv);
-        red_step_sm<S, NShared>(X, Y, hi, n, n0inv);
-        red_step_sm<S, NShared>(Y, X, hi, n, n0inv);
-        red_step_sm<S, NShared>(X, Y, hi, n, n0inv);
-        red_step_sm<S, NShared>(Y, X, hi, n, n0inv);
-        red_step_sm<S, NShared>(X, Y, hi, n, n0inv);
-        red_step_sm<S, NShared>(Y, X, hi, n, n0inv);
+    for (int i = 0; i < S; i += RSA_MULTI_RED) {
+#pragma unroll
+        for (int u = 0; u < RSA_MULTI_RED; u += 2) {
+            red_step_sm<S, NShared>(X, Y, hi, n, n0inv);
+            red_step_sm<S, NShared>(Y, X, hi, n, n0inv);
+        }
     }
     finish_sm<S, NShared>(a, X, Y, hi, T + S, n);
 }
