@@ -67,6 +67,9 @@ def parse():
     ap.add_argument("--count", type=int, default=0, help="override packets per rank (profiling only)")
     ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
                     help="process-group backend for N > 1 (gloo: test the multi-rank path on fewer GPUs)")
+    ap.add_argument("--kernel-path", action="append", default=[], metavar="S=PATH",
+                    help="A/B only: run width class S on another kernel (rsa_set_kernel_path), PATH one of "
+                         "fp64, int, int_group, int_pair, int_multi; e.g. --kernel-path 64=int")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=20.0, help="CPU-seconds budget of the oracle sample")
@@ -321,6 +324,9 @@ def run_ours(args, rank, world, local_rank):
 
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
+    for kp in args.kernel_path:
+        cls, path = kp.split("=")
+        R.rsa_set_kernel_path(int(cls), getattr(R, "RSA_PATH_" + path.upper()))
     key_name, total, legs = WORKLOADS[args.config]
     if args.count:
         total = args.count
@@ -595,6 +601,7 @@ def run_ours(args, rank, world, local_rank):
             "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f64" if fp64 else "u32", "data": "synthetic",
             "config": {"workload": args.config, "packets_total": total, "packets_per_rank": per,
+                       **({"kernel_path": args.kernel_path} if args.kernel_path else {}),
                        "key": key_name + " (seeded, "
                        "workload/keys.json)", "legs": [l for l, _ in legs], "modulus_bits": nb,
                        "l2": f"inputs {count * s * 4 / 2**20:.0f} MiB per leg vs 126 MB L2"
