@@ -67,9 +67,6 @@
 #ifndef RSA_F64_SQACC2
 #define RSA_F64_SQACC2 0   // recursive product scan: two partial sums per column sum (A/B)
 #endif
-#ifndef RSA_F64_SQCB
-#define RSA_F64_SQCB 0     // montsqr's product scan in column blocks of this width (0: column by column)
-#endif
 #ifndef RSA_F64_SQLOOP
 #define RSA_F64_SQLOOP 40  // product scan as plain unrolled loops up to this ND (ptxas stops unrolling
 #endif                     // the loop form at ND = 80: the recursive form expands at compile time)
@@ -576,63 +573,6 @@ __host__ __device__ __forceinline__ void montsqr(double (&a)[ND], const double* 
     // 1. T = A^2
     if constexpr (ND > RSA_F64_SQLOOP) {
         sqr_scan<ND>(a, [&](int kk, uint64_t v) { th[kk * stride] = v; });
-    } else if constexpr (RSA_F64_SQCB > 0) {
-        // column blocks of CB: for each block, the rows i add their products
-        // a_i a_j (i < j) into CB independent column accumulators (+1 for the
-        // high halves spilling into the next block) -- the reduction loop's
-        // dataflow (each product's low half paired with the previous one's
-        // high half in one 3-input add), no single serial chain per column
-        constexpr int CB = RSA_F64_SQCB;
-        uint64_t carry = 0, hd = 0;
-        uint64_t acc[CB + 1], xb[CB + 1];
-#pragma unroll
-        for (int c = 0; c <= CB; c++) { acc[c] = 0; xb[c] = 0; }
-#pragma unroll
-        for (int k0 = 0; k0 < 2 * ND; k0 += CB) {
-#pragma unroll
-            for (int i = 0; i < ND; i++) {
-                uint64_t hp = 0, hpb = 0;
-                int cprev = -1;
-#pragma unroll
-                for (int cc = 0; cc < CB; cc++) {
-                    const int j = k0 + cc - i;
-                    if (i < j && j < ND) {
-                        const double h = fma_rz(a[i], a[j], C104);
-                        const double l = fma_rz(a[i], a[j], sub_rn(C2, h));
-                        acc[cc] += bits(l) + hp;
-                        xb[cc] += BL + hpb;
-                        hp = bits(h);
-                        hpb = BH;
-                        cprev = cc;
-                    }
-                }
-                if (cprev >= 0) {              // the row's last high half: next column
-                    acc[cprev + 1] += hp;
-                    xb[cprev + 1] += hpb;
-                }
-            }
-#pragma unroll
-            for (int cc = 0; cc < CB && k0 + cc < 2 * ND; cc++) {
-                const int k = k0 + cc;
-                uint64_t y = hd, yb = (k > 0 && ((k - 1) & 1) == 0 && (k - 1) / 2 < ND) ? BH : 0;
-                hd = 0;
-                if ((k & 1) == 0 && k / 2 < ND) {
-                    const double ai = a[k / 2];
-                    const double h = fma_rz(ai, ai, C104);
-                    const double l = fma_rz(ai, ai, sub_rn(C2, h));
-                    y += bits(l);
-                    yb += BL;
-                    hd = bits(h);
-                }
-                const uint64_t v = 2 * (acc[cc] - xb[cc]) + (y - yb) + carry;
-                carry = v >> D;
-                th[k * stride] = v & M52;
-            }
-            acc[0] = acc[CB];
-            xb[0] = xb[CB];
-#pragma unroll
-            for (int c = 1; c <= CB; c++) { acc[c] = 0; xb[c] = 0; }
-        }
     } else {
         uint64_t carry = 0;
         uint64_t hx[ND], hd = 0;          // high halves pending for the next column (cross, diagonal)
