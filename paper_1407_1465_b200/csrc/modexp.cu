@@ -234,6 +234,9 @@ modexp_small_kernel(const __grid_constant__ ModexpParams<S> p) {
     V* const table = reinterpret_cast<V*>(p.table);
     const unsigned long long trips = (p.count + nvs - 1) / nvs;
     for (unsigned long long t = 0; t < trips; t++) {
+        // no barriers here: a thread with no packet left stops (its first slot is
+        // its lowest), so the last, partial wave leaves the SMs to the warps with work
+        if (t * nvs + gtid >= p.count) break;
         uint32_t a[PPT][S];
         unsigned long long pkt[PPT];
         bool valid[PPT];

@@ -48,6 +48,9 @@ namespace rsa_b200 {
 #ifndef RSA_F64_MINB32
 #define RSA_F64_MINB32 4
 #endif
+#ifndef RSA_F64_EARLYEXIT
+#define RSA_F64_EARLYEXIT 0   // non-lockstep classes: threads stop when the batch runs out (A/B: CRT-2048 2.14M vs 2.19M, off)
+#endif
 #ifndef RSA_F64_SQR128
 #define RSA_F64_SQR128 1    // 4096-bit kernel: dedicated squaring with A in its one slot (montsqr_slot)
 #endif
@@ -117,12 +120,18 @@ modexp_f64_kernel(const __grid_constant__ ModexpF64Params<S> p) {
         c104 = __longlong_as_double(__double_as_longlong(c104) + z);
     }
 
-    // every thread runs the same number of trips (uniform barriers); an
-    // out-of-range trip recomputes the last packet and skips the store
+    // Every thread runs the same number of trips (uniform barriers in the
+    // lockstep configurations); an out-of-range trip recomputes the last packet
+    // and skips the store.  Measured alternatives: guarding the arithmetic of
+    // such a trip (582K vs 591K at 2048 bits, and no faster on a partial last
+    // wave, whose packets sit on the first SMs anyway); stopping those threads
+    // in the non-lockstep 1024-bit class (RSA_F64_EARLYEXIT: CRT-2048 2.14M vs
+    // 2.19M).
     const unsigned long long trips = (ip.count + nthr - 1) / nthr;
     for (unsigned long long tr = 0; tr < trips; tr++) {
         const unsigned long long pkt0 = gtid + tr * nthr;
         const bool valid = pkt0 < ip.count;
+        if (RSA_F64_EARLYEXIT && !F64Cfg<S>::LOCKSTEP && !valid) break;
         const unsigned long long pkt = valid ? pkt0 : ip.count - 1;
         const uint32_t* src = ip.base + pkt * (unsigned long long)ip.s_io;
         auto load_input = [&](double (&x)[ND]) {

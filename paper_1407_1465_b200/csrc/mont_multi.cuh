@@ -207,10 +207,11 @@ __device__ __forceinline__ void montmul_sm(uint32_t (&a)[S], const uint4* __rest
     uint32_t X[S], Y[S], hi = 0;
 #pragma unroll
     for (int k = 0; k < S; k++) { X[k] = 0; Y[k] = 0; }
+    constexpr int MG = (RSA_MULTI_MUL < S ? RSA_MULTI_MUL : S) / 4;   // limb groups per loop trip
 #pragma unroll 1
-    for (int g0 = 0; g0 < S / 4; g0 += RSA_MULTI_MUL / 4) {
+    for (int g0 = 0; g0 < S / 4; g0 += MG) {
 #pragma unroll
-        for (int g = g0; g < g0 + RSA_MULTI_MUL / 4; g++) {
+        for (int g = g0; g < g0 + MG; g++) {
             const uint4 bv = bslot[g * stride];
             cios_step_sm<S, NShared>(X, Y, hi, a, bv.x, n, n0inv);
             cios_step_sm<S, NShared>(Y, X, hi, a, bv.y, n, n0inv);
@@ -229,11 +230,12 @@ __device__ __forceinline__ void montsqr_sm(uint32_t (&a)[S], const NShared& n, u
     uint32_t X[S], Y[S], hi = 0;
 #pragma unroll
     for (int k = 0; k < S; k++) { X[k] = T[k]; Y[k] = 0; }
-    // RSA_MULTI_RED: reduction steps per loop trip (A/B)
+    // RSA_MULTI_RED: reduction steps per loop trip (at most S)
+    constexpr int RED = RSA_MULTI_RED < S ? RSA_MULTI_RED : S;
 #pragma unroll 1
-    for (int i = 0; i < S; i += RSA_MULTI_RED) {
+    for (int i = 0; i < S; i += RED) {
 #pragma unroll
-        for (int u = 0; u < RSA_MULTI_RED; u += 2) {
+        for (int u = 0; u < RED; u += 2) {
             red_step_sm<S, NShared>(X, Y, hi, n, n0inv);
             red_step_sm<S, NShared>(Y, X, hi, n, n0inv);
         }
