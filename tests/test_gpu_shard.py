@@ -6,7 +6,8 @@ CUDA compute, bit-exact against the oracle element by element:
     each rank holds only its slice, the result is reassembled on every rank,
     the host entry returns it on rank 0;
   * several devices in one process (the per-device launch caches), when the
-    box has more than one GPU."""
+    box has more than one GPU;
+  * several host threads calling the C-ABI at once on their own streams."""
 import os
 import socket
 
@@ -116,3 +117,44 @@ def test_device_switch_in_one_process():
         x = torch.from_numpy(base.view(np.int32)).to(f"cuda:{dev}")
         got = R.rsa_modexp_batch(x, k["d"], k["n"], 2048).cpu().numpy().view(np.uint32)
         assert np.array_equal(got, want), dev
+
+
+def test_concurrent_calls_from_threads():
+    """Several host threads, each on its own CUDA stream with its own key and
+    width class, call the C-ABI at once: the plan cache, the per-device launch
+    caches and the stream-ordered workspaces are shared; every result stays
+    bit-exact."""
+    torch = _cuda()
+    import threading
+    import paper_1407_1465_b200 as R
+    jobs = [("rsa2048", 300), ("rsa1024", 500), ("rsa4096", 80), ("rsa64", 3000), ("rsa512", 700),
+            ("rsa2048", 301), ("toy17947", 999), ("rsa3072", 90)]
+    want, errors = {}, []
+    for idx, (key, count) in enumerate(jobs):
+        k = workload.key(key)
+        m = workload.packets(count, k["nbits"], n=k["n"], config_id=40 + idx)
+        want[idx] = (m, oracle.modexp_batch(m, k["d"], k["n"])[:, :m.shape[1]])
+    start = threading.Barrier(len(jobs))
+
+    def run(idx):
+        try:
+            key, _ = jobs[idx]
+            k = workload.key(key)
+            m, w = want[idx]
+            st = torch.cuda.Stream()
+            with torch.cuda.stream(st):
+                x = torch.from_numpy(m.view(np.int32)).cuda()
+                start.wait()
+                for _ in range(3):
+                    y = R.rsa_modexp_batch(x, k["d"], k["n"], k["nbits"], stream=st)
+                st.synchronize()
+            if not np.array_equal(y.cpu().numpy().view(np.uint32), w):
+                errors.append(idx)
+        except Exception as ex:            # surfaced below
+            errors.append((idx, repr(ex)))
+    ths = [threading.Thread(target=run, args=(i,)) for i in range(len(jobs))]
+    for t in ths:
+        t.start()
+    for t in ths:
+        t.join()
+    assert not errors, errors
