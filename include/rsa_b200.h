@@ -248,6 +248,10 @@ int rsa_set_window(int w);
  *   RSA_PATH_INT_GROUP  S = 64: 2 lanes per packet; S = 128: 4 lanes
  *   RSA_PATH_INT_PAIR   S = 128: 2 lanes per packet
  *   RSA_PATH_INT_MULTI  S = 2, 4: several packets per thread (default there)
+ *   RSA_PATH_TC         S = 64: the product A B on the FP64 pipe, the
+ *                       Montgomery reduction (m = T n' mod R, T + m n) as u8
+ *                       matrix products on the tensor core (tcgen05, TMEM),
+ *                       R = 2^2048; 128-packet tiles, one CTA per SM
  * rsa_set_kernel_path sets the path of class `width_class` for subsequent
  * calls of every thread (process-wide, thread-safe; a call in flight keeps the
  * path it started with).  RSA_PATH_DEFAULT restores the default, under which
@@ -262,6 +266,7 @@ int rsa_set_window(int w);
 #define RSA_PATH_INT_GROUP  3
 #define RSA_PATH_INT_PAIR   4
 #define RSA_PATH_INT_MULTI  5
+#define RSA_PATH_TC         6
 int rsa_set_kernel_path(int width_class, int path);
 int rsa_get_kernel_path(int width_class);
 

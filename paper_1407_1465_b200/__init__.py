@@ -41,7 +41,7 @@ EXPORTS = ["rsa_strerror", "rsa_keygen_check", "rsa_validate_key", "rsa_modexp_b
 # kernel paths per width class (rsa_set_kernel_path; include/rsa_b200.h)
 # the paper's single-word schedules (rsa_modexp_batch_schedule)
 RSA_SCHED_NAIVE, RSA_SCHED_R2L, RSA_SCHED_L2R, RSA_SCHED_HALVING, RSA_SCHED_HALVING_FAITHFUL = 1, 2, 3, 4, 5
-RSA_PATH_DEFAULT, RSA_PATH_FP64, RSA_PATH_INT, RSA_PATH_INT_GROUP, RSA_PATH_INT_PAIR, RSA_PATH_INT_MULTI = range(6)
+RSA_PATH_DEFAULT, RSA_PATH_FP64, RSA_PATH_INT, RSA_PATH_INT_GROUP, RSA_PATH_INT_PAIR, RSA_PATH_INT_MULTI, RSA_PATH_TC = range(7)
 
 if not os.path.exists(LIB_PATH):
     raise ImportError(f"{LIB_PATH} is not built: run `python paper_1407_1465_b200/build.py` "

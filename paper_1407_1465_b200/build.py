@@ -8,8 +8,8 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "librsa_b200.so")
-SOURCES = [os.path.join(CSRC, f) for f in ("modexp.cu", "modexp_f64.cu", "modexp_multi.cu", "crt.cu", "rsa_abi.cpp")]
-DEPS = SOURCES + [os.path.join(CSRC, f) for f in ("mont.cuh", "mont_f64.cuh", "mont_pair.cuh", "mont_sqr.cuh", "mont_multi.cuh", "mont_group.cuh", "plan.h", "host_bn.hpp", "devcache.h")] + [
+SOURCES = [os.path.join(CSRC, f) for f in ("modexp.cu", "modexp_f64.cu", "modexp_tc.cu", "modexp_multi.cu", "crt.cu", "rsa_abi.cpp")]
+DEPS = SOURCES + [os.path.join(CSRC, f) for f in ("mont.cuh", "mont_f64.cuh", "mont_pair.cuh", "mont_sqr.cuh", "mont_multi.cuh", "mont_group.cuh", "mont_tc.cuh", "tc_i8.cuh", "tc_digits.cuh", "plan.h", "host_bn.hpp", "devcache.h")] + [
     os.path.join(os.path.dirname(HERE), "include", "rsa_b200.h")]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]

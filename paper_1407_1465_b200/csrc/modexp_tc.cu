@@ -1,0 +1,214 @@
+// modexp_tc.cu -- batched modular exponentiation with the Montgomery
+// reduction on the tensor core (sm_100a), width class S = 64 (1025..2048-bit
+// moduli).
+//
+// Same contract and op list as modexp_kernel / modexp_f64_kernel: out[i] =
+// base[i]^exp mod n for every packet (sec. 2, sec.
+// 3.3), one thread per packet, the shared exponent's op list executed
+// warp-uniformly.  Each Montgomery multiply A <- A B R^-1 mod n (R = 2^2048)
+// is split between the two engines of the SM:
+//   CUDA cores (FP64 pipe): T = A B by product scanning (tc_digits.cuh;
+//     squarings by f64::sqr_scan, ND (ND+1)/2 = 820 digit products instead of
+//     the 2420 of a full FP64 Montgomery squaring), streamed out as words:
+//     T_low into the tile's staging buffer, T_high into registers;
+//   tensor core: m = T_low n' mod R and the columns of m n (mont_tc.cuh),
+//     the carries resolved by each packet's thread; U < n after one
+//     conditional subtraction (so every intermediate is canonical).
+// CTA = two tiles of 128 packets (warps 0-3, 4-7), one CTA per SM (255
+// registers): while one tile waits for its MMAs the other one's warps run.
+// Each tile owns 256 TMEM columns and a mbarrier; the tiles synchronise
+// only with named barriers of their own 128 threads.
+//
+// Shared memory: TcShared (n' and n Toeplitz strips, 2 x 32 KB staging) and a
+// per-thread B slot (ND doubles, digit-major across the block) for the
+// multiplies' second operand.  The window table is the FP64 kernel's format
+// (entries as digit pairs, entry-major then pair-major across the grid).
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "devcache.h"
+#include "mont_tc.cuh"
+#include "plan.h"
+#include "tc_digits.cuh"
+
+namespace rsa_b200 {
+
+constexpr int TC_S = 64;
+constexpr int TC_ND = rsa_f64_digits(TC_S);    // 40 digits of 52 bits (A < n < 2^2048)
+constexpr int TC_BLOCK = 256;
+static_assert(TC_ND == 40, "2048-bit class");
+
+__global__ void __launch_bounds__(TC_BLOCK, 1) modexp_tc_kernel(const __grid_constant__ ModexpTcParams<TC_S> p) {
+    constexpr int ND = TC_ND, NP = ND / 2, NW = tc::NW;
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    tc::TcShared& sh = *reinterpret_cast<tc::TcShared*>(smem_raw);
+    double* const bslot = reinterpret_cast<double*>(smem_raw + sizeof(tc::TcShared)) + threadIdx.x;
+    __shared__ __align__(16) double r2d[ND];
+    const ModexpParams<TC_S>& ip = p.f.ip;
+    const int warp = threadIdx.x / 32;
+    if (warp == 0) tc::tmem_alloc(tc::smem_u32(&sh.tmem_base), 512);
+    if (threadIdx.x == 0) {
+        tc::mbar_init(tc::smem_u32(&sh.mbar[0]), 1);
+        tc::mbar_init(tc::smem_u32(&sh.mbar[1]), 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    tc::build_strips(sh, p.npb, reinterpret_cast<const uint8_t*>(ip.n));
+    for (int i = threadIdx.x; i < NW; i += blockDim.x) sh.nw[i] = ip.n[i];
+    if (threadIdx.x < 32) {
+        double d[ND];
+        tcd::words_to_digits<ND>([&](int w) -> uint32_t { return w < TC_S ? ip.r2[w] : 0u; }, d);
+        for (int k = threadIdx.x; k < ND; k += 32) r2d[k] = d[k];
+    }
+    tc::fence_before();
+    __syncthreads();
+    tc::fence_after();
+    tc::TcTile tt;
+    tt.tile = threadIdx.x / tc::TILE;
+    tt.r = threadIdx.x % tc::TILE;
+    tt.tmem = sh.tmem_base + 256 * tt.tile;
+    tt.tlane = (uint32_t)(32 * (warp % 4)) << 16;
+    tt.mbar = tc::smem_u32(&sh.mbar[tt.tile]);
+    tt.phase = 0;
+
+    const unsigned gtid = blockIdx.x * blockDim.x + threadIdx.x;
+    const unsigned nthr = gridDim.x * blockDim.x;
+    double2* const table = reinterpret_cast<double2*>(ip.table);
+    // every thread runs the same trips (the tiles' barriers); an out-of-range
+    // trip recomputes the last packet and skips the store
+    const unsigned long long trips = (ip.count + nthr - 1) / nthr;
+    for (unsigned long long tr = 0; tr < trips; tr++) {
+        const unsigned long long pkt0 = gtid + tr * nthr;
+        const bool valid = pkt0 < ip.count;
+        const unsigned long long pkt = valid ? pkt0 : ip.count - 1;
+        const uint32_t* src = ip.base + pkt * (unsigned long long)ip.s_io;
+        auto load_input = [&](double (&x)[ND]) {
+            uint32_t l[TC_S];
+            if (ip.s_io == TC_S) {
+#pragma unroll
+                for (int k = 0; k < TC_S; k += 4) {
+                    const uint4 v = __ldg(reinterpret_cast<const uint4*>(src + k));
+                    l[k] = v.x; l[k + 1] = v.y; l[k + 2] = v.z; l[k + 3] = v.w;
+                }
+            } else {
+#pragma unroll
+                for (int k = 0; k < TC_S; k++) l[k] = (k < ip.s_io) ? __ldg(src + k) : 0u;
+            }
+            tcd::words_to_digits<ND>([&](int w) -> uint32_t { return w < TC_S ? l[w] : 0u; }, x);
+        };
+        double a[ND];
+        uint32_t th[NW];
+        load_input(a);
+
+        for (int i = 0; i < ip.nops; i++) {
+            const RsaOp op = ip.ops[i];
+            if (op.flags & RSA_F_LOADA) {
+#pragma unroll
+                for (int g = 0; g < NP; g++) {
+                    const double2 v = table[((size_t)op.lidx * NP + g) * nthr + gtid];
+                    a[2 * g] = v.x;
+                    a[2 * g + 1] = v.y;
+                }
+            }
+            // the second operand of a multiply goes to this thread's slot
+            if (op.kind == RSA_OP_MUL) {
+#pragma unroll
+                for (int g = 0; g < NP; g++) {
+                    const double2 v = table[((size_t)op.bidx * NP + g) * nthr + gtid];
+                    bslot[(2 * g) * TC_BLOCK] = v.x;
+                    bslot[(2 * g + 1) * TC_BLOCK] = v.y;
+                }
+            } else if (op.kind == RSA_OP_R2) {
+#pragma unroll
+                for (int k = 0; k < ND; k++) bslot[k * TC_BLOCK] = r2d[k];
+            } else if (op.kind == RSA_OP_MULX) {
+                double x[ND];
+                load_input(x);
+#pragma unroll
+                for (int k = 0; k < ND; k++) bslot[k * TC_BLOCK] = x[k];
+            } else if (op.kind == RSA_OP_ONE) {
+#pragma unroll
+                for (int k = 0; k < ND; k++) bslot[k * TC_BLOCK] = (k == 0) ? 1.0 : 0.0;
+            }
+            for (int r = 0; r < op.rep; r++) {
+                // T = A B: words 0..63 to the staging buffer (16-byte chunks), 64..127 to th
+                uint32_t t63 = 0, wb0 = 0, wb1 = 0, wb2 = 0;
+                auto word = [&](int w, uint32_t v) {
+                    if (w < NW) {
+                        if ((w & 3) == 0) wb0 = v;
+                        else if ((w & 3) == 1) wb1 = v;
+                        else if ((w & 3) == 2) wb2 = v;
+                        else *tc::stage_chunk(sh, tt.tile, tt.r, w >> 2) = make_uint4(wb0, wb1, wb2, v);
+                        if (w == NW - 1) t63 = v;
+                    } else {
+                        th[w - NW] = v;
+                    }
+                };
+                tcd::Packer<2 * NW, decltype(word)> pk{word, 0};
+                auto put = [&](int k, uint64_t d) { pk.put(k, d); };
+                if (op.kind == RSA_OP_SQR) {
+                    f64::sqr_scan<ND>(a, put);
+                } else {
+                    auto bget = [&](int j) -> double { return f64::ld_digit(bslot + j * TC_BLOCK); };
+                    tcd::mul_scan<ND>(a, bget, put);
+                }
+                tc::redc(sh, tt, t63, th);
+                tcd::words_to_digits<ND>([&](int w) -> uint32_t { return w < NW ? th[w] : 0u; }, a);
+            }
+            if (op.flags & RSA_F_STORE) {
+#pragma unroll
+                for (int g = 0; g < NP; g++)
+                    table[((size_t)op.sidx * NP + g) * nthr + gtid] = make_double2(a[2 * g], a[2 * g + 1]);
+            }
+        }
+        // the last op (RSA_OP_ONE or RSA_OP_MULX) left the canonical result in th
+        uint32_t* dst = ip.out + pkt * (unsigned long long)ip.s_io;
+        if (!valid) {
+        } else if (ip.s_io == TC_S) {
+#pragma unroll
+            for (int k = 0; k < TC_S; k += 4)
+                *reinterpret_cast<uint4*>(dst + k) = make_uint4(th[k], th[k + 1], th[k + 2], th[k + 3]);
+        } else {
+#pragma unroll
+            for (int k = 0; k < TC_S; k++)
+                if (k < ip.s_io) dst[k] = th[k];
+        }
+    }
+    tc::fence_before();
+    __syncthreads();
+    if (warp == 0) {
+        tc::fence_after();
+        tc::tmem_dealloc(sh.tmem_base, 512);
+    }
+}
+
+static size_t tc_smem_bytes() { return sizeof(tc::TcShared) + sizeof(double) * TC_ND * TC_BLOCK; }
+
+static cudaError_t launch_tc(const void* params, int sms, cudaStream_t stream, int* grid_out, int* block_out,
+                             size_t* slots_out, bool query_only) {
+    const int block = TC_BLOCK;
+    const size_t smem = tc_smem_bytes();
+    static OccCache cache;
+    int occ = 0;
+    cudaError_t ce = cached_occupancy(
+        cache, [&](int* o) { return occupancy_with_smem(modexp_tc_kernel, block, smem, o); }, &occ);
+    if (ce != cudaSuccess) return ce;
+    if (occ > 1) occ = 1;   // one CTA per SM: each CTA allocates all 512 TMEM columns
+    int grid = sms * occ;
+    if (grid_out) *grid_out = grid;
+    if (block_out) *block_out = block;
+    if (slots_out) *slots_out = (size_t)grid * block;
+    if (query_only) return cudaSuccess;
+    const ModexpTcParams<TC_S>& prm = *static_cast<const ModexpTcParams<TC_S>*>(params);
+    const unsigned long long need = (prm.f.ip.count + block - 1) / block;
+    if (need < (unsigned long long)grid) grid = (int)need;
+    modexp_tc_kernel<<<grid, block, smem, stream>>>(prm);
+    return cudaGetLastError();
+}
+
+}  // namespace rsa_b200
+
+cudaError_t rsa_b200_launch_tc(int S, const void* params, int sms, cudaStream_t stream, int* grid, int* block,
+                               size_t* slots, bool query_only) {
+    if (S != rsa_b200::TC_S) return cudaErrorInvalidValue;
+    return rsa_b200::launch_tc(params, sms, stream, grid, block, slots, query_only);
+}

@@ -1,0 +1,219 @@
+// mont_tc.cuh -- Montgomery reduction of a 128-packet tile on the tensor core
+// (2048-bit class: R = 2^2048, n < R odd, byte digits for the MMAs).
+//
+// The operation is the reduction half of Fig 3's "(u*v) mod m" (PAPER.md:89,
+// sec. 3.6.1) realised by Montgomery's method, in
+// separated form with a FULL-WIDTH quotient:
+//
+//   T = A B  (< n R, computed on the CUDA cores by the caller)
+//   m = (T mod R) n' mod R,            n' = -n^-1 mod R
+//   U = (T + m n) / R  (< 2n),   U -= n if U >= n   ->   U = A B R^-1 mod n
+//
+// Both products have a constant operand (n', n: one key per batch), so for a
+// tile of 128 packets they are [128 x 256] x [256 x N] u8 matrix products on
+// the tensor core (tc_i8.cuh) against Toeplitz matrices, read out of TMEM as
+// exact column sums c_j = sum_k x_k y_{j-k} (< 2^24) whose carries the
+// thread of each packet resolves:
+//   GEMM1: columns 0..255 of T_low x n'   (two N = 128 blocks; the upper
+//          block-triangle is zero and skipped: 12 MMAs of K = 32)
+//   GEMM2: columns 252..507 of m x n       (8 MMAs, N = 256); columns
+//          508..510 (6 byte products) on the CUDA cores.
+// The carry out of the low half of T + m n: its value V = (T_low + sum_{j<256}
+// c_j 2^(8j)) / R is an integer (T + m n = 0 mod R), and columns below 252
+// move V 2^32 by less than 2^17 (c_j < 2^24), so V = ceil(X / 2^32) with
+// X = T_low's top word + c_252 + c_253 2^8 + c_254 2^16 + c_255 2^24.
+//
+// Shared memory (per CTA of two tiles): the n' and n "strips" (every
+// Toeplitz block is a row window of one strip, see tc_i8.cuh), and per tile a
+// 128 x 256-byte staging buffer holding T_low, then m (A operand of both
+// GEMMs).  TMEM: 256 columns per tile (GEMM1 and GEMM2 reuse them).
+#pragma once
+#include <stdint.h>
+
+#include "tc_i8.cuh"
+
+namespace rsa_b200 {
+namespace tc {
+
+constexpr int KB = 256;                       // bytes per operand (R = 2^2048)
+constexpr int NW = 64;                        // 32-bit words per operand
+constexpr int TILE = 128;                     // packets per tile (MMA M, TMEM lanes)
+constexpr int STAGE_LBO = TILE * 16;          // bytes between 16-byte K chunks of a staging buffer
+constexpr int STAGE_BYTES = KB / 16 * STAGE_LBO;   // 32 KB
+// n' strip: GEMM1 blocks c0 in {0, 128}, K blocks I <= (c0 + 127) / 32: rows
+// rho = c0 + nn - 32 I in [-96, 255]
+constexpr int NP_RHO0 = -96, NP_ROWS = 352, NP_LBO = NP_ROWS * 16;
+// n strip: GEMM2 c0 = 252, I = 0..7: rows [28, 507]
+constexpr int G2_C0 = 252;
+constexpr int N_RHO0 = G2_C0 - 224, N_ROWS = 480, N_LBO = N_ROWS * 16;
+constexpr int NP_STRIP_BYTES = 2 * NP_LBO, N_STRIP_BYTES = 2 * N_LBO;
+
+struct __align__(16) TcShared {
+    uint8_t stage[2][STAGE_BYTES];            // per tile: T_low, then m
+    uint8_t np_strip[NP_STRIP_BYTES];
+    uint8_t n_strip[N_STRIP_BYTES];
+    uint32_t nw[NW];                          // n as words (conditional subtraction)
+    unsigned long long mbar[2];
+    uint32_t tmem_base;
+};
+
+// strip byte (chunk q, row rho, byte b) = y_{rho - 16 q - b} (0 outside [0, 256))
+__device__ __forceinline__ void build_strips(TcShared& sh, const uint8_t* __restrict__ npb,
+                                             const uint8_t* __restrict__ nb) {
+    for (int i = threadIdx.x; i < NP_STRIP_BYTES; i += blockDim.x) {
+        const int q = i / NP_LBO, rem = i % NP_LBO, rho = rem / 16 + NP_RHO0, b = rem % 16;
+        const int idx = rho - 16 * q - b;
+        sh.np_strip[i] = (idx >= 0 && idx < KB) ? npb[idx] : 0;
+    }
+    for (int i = threadIdx.x; i < N_STRIP_BYTES; i += blockDim.x) {
+        const int q = i / N_LBO, rem = i % N_LBO, rho = rem / 16 + N_RHO0, b = rem % 16;
+        const int idx = rho - 16 * q - b;
+        sh.n_strip[i] = (idx >= 0 && idx < KB) ? nb[idx] : 0;
+    }
+}
+
+// staging address of 16-byte chunk c (bytes 16c .. 16c+15) of tile row r
+__device__ __forceinline__ uint4* stage_chunk(TcShared& sh, int tile, int r, int c) {
+    return reinterpret_cast<uint4*>(sh.stage[tile] + c * STAGE_LBO + r * 16);
+}
+
+__device__ __forceinline__ void issue_gemm1(TcShared& sh, int tile, uint32_t tmem) {
+    const uint32_t st = smem_u32(sh.stage[tile]), sp = smem_u32(sh.np_strip);
+    constexpr uint32_t id = idesc_u8(128, 128);
+#pragma unroll
+    for (int blk = 0; blk < 2; blk++) {
+        const int c0 = 128 * blk;
+#pragma unroll
+        for (int I = 0; I < 4 + 4 * blk; I++) {
+            const uint64_t a = sdesc(st + 2 * I * STAGE_LBO, STAGE_LBO, 128);
+            const uint64_t b = sdesc(sp + (c0 - 32 * I - NP_RHO0) * 16, NP_LBO, 128);
+            mma_u8(tmem + c0, a, b, id, I > 0);
+        }
+    }
+}
+
+__device__ __forceinline__ void issue_gemm2(TcShared& sh, int tile, uint32_t tmem) {
+    const uint32_t st = smem_u32(sh.stage[tile]), sn = smem_u32(sh.n_strip);
+    constexpr uint32_t id = idesc_u8(128, 256);
+#pragma unroll
+    for (int I = 0; I < 8; I++) {
+        const uint64_t a = sdesc(st + 2 * I * STAGE_LBO, STAGE_LBO, 128);
+        const uint64_t b = sdesc(sn + (G2_C0 - 32 * I - N_RHO0) * 16, N_LBO, 128);
+        mma_u8(tmem, a, b, id, I > 0);
+    }
+}
+
+// 4 column sums at byte offsets 0, 8, 16, 24 of a word, plus the carry in
+__device__ __forceinline__ uint64_t col4(uint32_t c0, uint32_t c1, uint32_t c2, uint32_t c3) {
+    return (uint64_t)c0 + ((uint64_t)c1 << 8) + ((uint64_t)c2 << 16) + ((uint64_t)c3 << 24);
+}
+
+// Per-thread state of the reduction: the tile's TMEM columns and mbarrier phase.
+struct TcTile {
+    int tile;          // 0 or 1
+    int r;             // row in the tile (0..127) = TMEM lane
+    uint32_t tmem;     // this tile's first TMEM column (lane 0)
+    uint32_t tlane;    // this warp's lane offset (32 (warp % 4)) << 16
+    uint32_t mbar;
+    uint32_t phase;
+};
+
+// U = (T + m n) / R reduced below n.  On entry T_low (words 0..63) is in the
+// tile's staging buffer (written by this thread, generic proxy), t63 = its top
+// word, th[] = T_high (words 64..127).  On exit th[] holds U < n.
+__device__ __forceinline__ void redc(TcShared& sh, TcTile& tt, uint32_t t63, uint32_t (&th)[NW]) {
+    const int tile = tt.tile, r = tt.r;
+    // ---- GEMM1: m's column sums
+    fence_async_smem();
+    fence_before();
+    bar_sync(1 + tile, TILE);
+    if (r == 0) {
+        fence_after();
+        issue_gemm1(sh, tile, tt.tmem);
+        commit(tt.mbar);
+    }
+    mbar_wait(tt.mbar, tt.phase);
+    tt.phase ^= 1;
+    fence_after();
+    uint64_t carry = 0;
+    uint32_t m254 = 0, m255 = 0, m253 = 0;
+#pragma unroll
+    for (int ch = 0; ch < 8; ch++) {
+        uint32_t v[32];
+        tmem_ld32(tt.tmem + tt.tlane + 32 * ch, v);
+        tmem_ld_wait();
+        uint32_t w[8];
+#pragma unroll
+        for (int q = 0; q < 8; q++) {
+            const uint64_t s = carry + col4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+            w[q] = (uint32_t)s;
+            carry = s >> 32;
+        }
+        *stage_chunk(sh, tile, r, 2 * ch) = make_uint4(w[0], w[1], w[2], w[3]);
+        *stage_chunk(sh, tile, r, 2 * ch + 1) = make_uint4(w[4], w[5], w[6], w[7]);
+        if (ch == 7) {
+            m253 = (w[7] >> 8) & 0xFF;
+            m254 = (w[7] >> 16) & 0xFF;
+            m255 = w[7] >> 24;
+        }
+    }
+    // ---- GEMM2: columns 252..507 of m n
+    fence_async_smem();
+    fence_before();
+    bar_sync(1 + tile, TILE);
+    if (r == 0) {
+        fence_after();
+        issue_gemm2(sh, tile, tt.tmem);
+        commit(tt.mbar);
+    }
+    // columns 508..510 (the top byte products) meanwhile
+    const uint32_t n253 = sh.nw[63] >> 8 & 0xFF, n254 = sh.nw[63] >> 16 & 0xFF, n255 = sh.nw[63] >> 24;
+    const uint32_t c508 = m253 * n255 + m254 * n254 + m255 * n253;
+    const uint32_t c509 = m254 * n255 + m255 * n254;
+    const uint32_t c510 = m255 * n255;
+    mbar_wait(tt.mbar, tt.phase);
+    tt.phase ^= 1;
+    fence_after();
+#pragma unroll
+    for (int ch = 0; ch < 8; ch++) {
+        uint32_t v[32];
+        tmem_ld32(tt.tmem + tt.tlane + 32 * ch, v);
+        tmem_ld_wait();
+        // TMEM column idx = global column 252 + idx; word w of U (bits 2048 + 32 w)
+        // covers global columns 256 + 4w .. 259 + 4w = idx 4 + 4w .. 7 + 4w
+        if (ch == 0) {
+            const uint64_t x = (uint64_t)t63 + col4(v[0], v[1], v[2], v[3]);
+            carry = (x + 0xFFFFFFFFull) >> 32;
+        }
+#pragma unroll
+        for (int q = 0; q < 8; q++) {
+            const int w = 8 * ch + q - 1;          // word whose columns start at idx 32 ch + 4 q
+            if (w < 0) continue;
+            const uint64_t s = col4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]) + carry + th[w];
+            th[w] = (uint32_t)s;
+            carry = s >> 32;
+        }
+    }
+    // word 63 = columns 508..511 (idx 256..259, past the last chunk)
+    {
+        const uint64_t s = col4(c508, c509, c510, 0) + carry + th[NW - 1];
+        th[NW - 1] = (uint32_t)s;
+        carry = s >> 32;
+    }
+    // U < 2n: subtract n once if U >= n (U's bit 2048 is `carry`): the borrow
+    // chain of U - n decides, then the subtraction runs under a mask
+    uint32_t borrow = 0;
+#pragma unroll
+    for (int w = 0; w < NW; w++) borrow = (uint32_t)(((uint64_t)th[w] - sh.nw[w] - borrow) >> 32) & 1;
+    const uint32_t mask = (carry != 0 || borrow == 0) ? 0xFFFFFFFFu : 0u;
+    borrow = 0;
+#pragma unroll
+    for (int w = 0; w < NW; w++) {
+        const uint64_t s = (uint64_t)th[w] - (sh.nw[w] & mask) - borrow;
+        th[w] = (uint32_t)s;
+        borrow = (uint32_t)(s >> 32) & 1;
+    }
+}
+
+}  // namespace tc
+}  // namespace rsa_b200

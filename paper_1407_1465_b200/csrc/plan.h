@@ -81,6 +81,16 @@ struct ModexpF64Params {
     unsigned long long nu[rsa_f64_digits(S)];  // n, digits as integers (final subtraction)
 };
 
+// Tensor-core reduction kernel (modexp_tc.cu, class S = 64): R = 2^(32 S)
+// (ip.r2 is R^2 mod n for that R), the full-width quotient multiplier
+// n' = -n^-1 mod R as bytes for the tensor-core Toeplitz operand.  The FP64
+// params come first (same op list, same table entry format: digits as doubles).
+template <int S>
+struct ModexpTcParams {
+    ModexpF64Params<S> f;
+    uint8_t npb[4 * S];                      // -n^-1 mod 2^(32 S), little-endian bytes
+};
+
 // host-visible summary of a plan (also exported through the C-ABI)
 struct RsaPlanInfo {
     int width_class;              // S

@@ -192,9 +192,37 @@ static void fill_f64(ModexpF64Params<S>* f, const BN& n) {
     f->c104 = 20282409603651670423947251286016.0;     // 2^104
 }
 
+// the tensor-core kernel's quotient multiplier n' = -n^-1 mod 2^(32 S), as
+// bytes (Newton: x <- x (2 - n x) doubles the correct low bits per step)
+template <int S>
+static void fill_tc(ModexpTcParams<S>* t, const BN& n) {
+    BN R = rsa_host::shl(rsa_host::from_u64(1), 32 * S);
+    auto mod_r = [&](BN x) {
+        if ((int)x.size() > S) x.resize(S);
+        rsa_host::trim(x);
+        return x;
+    };
+    BN x = rsa_host::from_u64(1);
+    for (int bitsok = 1; bitsok < 32 * S; bitsok *= 2) {
+        BN nx = mod_r(rsa_host::mul(n, x));
+        BN two_minus = mod_r(rsa_host::sub(rsa_host::add(R, rsa_host::from_u64(2)), nx));   // 2 - n x mod R
+        x = mod_r(rsa_host::mul(x, two_minus));
+    }
+    BN npr = rsa_host::is_zero(x) ? x : rsa_host::sub(R, x);   // -n^-1 mod R
+    uint32_t w[S];
+    rsa_host::to_limbs(npr, w, S);
+    for (int i = 0; i < S; i++)
+        for (int b = 0; b < 4; b++) t->npb[4 * i + b] = (uint8_t)(w[i] >> (8 * b));
+}
+
 template <int S>
 static void fill_params(Plan& pl, const BN& n, const std::vector<RsaOp>& ops) {
-    if constexpr (S == 64 || S == 32 || S == 128) {
+    if constexpr (S == 64) {
+        // FP64 params + the tensor-core kernel's n' (one blob serves every path of the class)
+        pl.params.assign(sizeof(ModexpTcParams<S>), 0);
+        fill_f64<S>(reinterpret_cast<ModexpF64Params<S>*>(pl.params.data()), n);
+        if (pl.path == RSA_PATH_TC) fill_tc<S>(reinterpret_cast<ModexpTcParams<S>*>(pl.params.data()), n);
+    } else if constexpr (S == 32 || S == 128) {
         pl.params.assign(sizeof(ModexpF64Params<S>), 0);
         fill_f64<S>(reinterpret_cast<ModexpF64Params<S>*>(pl.params.data()), n);
     } else {
@@ -656,6 +684,12 @@ int rsa_plan_info(const uint32_t* exp, const uint32_t* n, int nbits, rsa_plan_in
         info->fp64_digits = (int)nd;
         const long long sqd = info->sqr_kernel ? nd * (nd + 1) / 2 + nd * nd : 2 * nd * nd;
         info->digit_products = pl.squarings * sqd + (pl.montmuls - pl.squarings) * 2 * nd * nd;
+    } else if (pl.path == RSA_PATH_TC) {
+        // CUDA-core digit products only (the product T = A B); the reduction's
+        // byte products run on the tensor core
+        const long long nd = rsa_f64_digits(pl.S);
+        info->fp64_digits = (int)nd;
+        info->digit_products = pl.squarings * (nd * (nd + 1) / 2) + (pl.montmuls - pl.squarings) * nd * nd;
     }
     const int sms = device_sms();
     if (sms) {

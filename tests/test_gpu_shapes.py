@@ -40,7 +40,8 @@ def _classes(key):
     return next(c for c in (2, 4, 8, 16, 32, 64, 128) if s <= c)
 
 
-@pytest.mark.parametrize("path,key,count", [("INT", "rsa2048", 300), ("INT", "rsa1536", 300),
+@pytest.mark.parametrize("path,key,count", [("TC", "rsa2048", 300), ("TC", "rsa1536", 300),
+                                            ("INT", "rsa2048", 300), ("INT", "rsa1536", 300),
                                             ("INT", "rsa1024", 300), ("FP64", "rsa1024", 300),
                                             ("FP64", "rsa2048", 300), ("FP64", "rsa1536", 300),
                                             ("INT_GROUP", "rsa2048", 300), ("INT_GROUP", "rsa1536", 300),
@@ -59,7 +60,7 @@ def test_alternative_shapes(path, key, count):
     with R.kernel_path(S, code):
         assert R.rsa_get_kernel_path(S) == code
         info = R.rsa_plan_info(workload.key(key)["d"], workload.key(key)["n"], workload.key(key)["nbits"])
-        assert (info["fp64_digits"] > 0) == (path == "FP64")
+        assert (info["fp64_digits"] > 0) == (path in ("FP64", "TC"))
         _check(key, count)
 
 
