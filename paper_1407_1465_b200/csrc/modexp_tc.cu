@@ -148,8 +148,12 @@ __global__ void __launch_bounds__(TC_BLOCK, 1) modexp_tc_kernel(const __grid_con
                 if (op.kind == RSA_OP_SQR) {
                     f64::sqr_scan<ND>(a, put);
                 } else {
+                    // rows, rolled (the unrolled column scan is ~160 KB of code);
+                    // T's low digits go back into b's slot as b's digits are used up
                     auto bget = [&](int j) -> double { return f64::ld_digit(bslot + j * TC_BLOCK); };
-                    tcd::mul_scan<ND>(a, bget, put);
+                    auto lout = [&](int j, uint64_t d) { reinterpret_cast<uint64_t*>(bslot)[j * TC_BLOCK] = d; };
+                    auto lin = [&](int j) -> uint64_t { return reinterpret_cast<const uint64_t*>(bslot)[j * TC_BLOCK]; };
+                    tcd::mul_rows<ND>(a, bget, lout, lin, put);
                 }
                 tc::redc(sh, tt, t63, th);
                 tcd::words_to_digits<ND>([&](int w) -> uint32_t { return w < NW ? th[w] : 0u; }, a);

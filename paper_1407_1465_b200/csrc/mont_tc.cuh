@@ -103,9 +103,39 @@ __device__ __forceinline__ void issue_gemm2(TcShared& sh, int tile, uint32_t tme
     }
 }
 
-// 4 column sums at byte offsets 0, 8, 16, 24 of a word, plus the carry in
+// 4 column sums at byte offsets 0, 8, 16, 24 of a word (independent per
+// word: three IMAD.WIDE; the carries between words are resolved afterwards by
+// one add-with-carry per word)
 __device__ __forceinline__ uint64_t col4(uint32_t c0, uint32_t c1, uint32_t c2, uint32_t c3) {
     return (uint64_t)c0 + ((uint64_t)c1 << 8) + ((uint64_t)c2 << 16) + ((uint64_t)c3 << 24);
+}
+
+// carry-chain steps (PTX condition code; consecutive volatile asm statements,
+// nothing between them writes CC)
+__device__ __forceinline__ uint32_t add_cc(uint32_t a, uint32_t b) {
+    uint32_t r;
+    asm volatile("add.cc.u32 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(b));
+    return r;
+}
+__device__ __forceinline__ uint32_t addc_cc(uint32_t a, uint32_t b) {
+    uint32_t r;
+    asm volatile("addc.cc.u32 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(b));
+    return r;
+}
+__device__ __forceinline__ uint32_t addc(uint32_t a, uint32_t b) {
+    uint32_t r;
+    asm volatile("addc.u32 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(b));
+    return r;
+}
+__device__ __forceinline__ uint32_t sub_cc(uint32_t a, uint32_t b) {
+    uint32_t r;
+    asm volatile("sub.cc.u32 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(b));
+    return r;
+}
+__device__ __forceinline__ uint32_t subc_cc(uint32_t a, uint32_t b) {
+    uint32_t r;
+    asm volatile("subc.cc.u32 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(b));
+    return r;
 }
 
 // Per-thread state of the reduction: the tile's TMEM columns and mbarrier phase.
@@ -121,6 +151,9 @@ struct TcTile {
 // U = (T + m n) / R reduced below n.  On entry T_low (words 0..63) is in the
 // tile's staging buffer (written by this thread, generic proxy), t63 = its top
 // word, th[] = T_high (words 64..127).  On exit th[] holds U < n.
+// Carries: word w of a GEMM's output is P_w = sum_i c_{4w+i} 2^(8i) < 2^50,
+// computed for 8 words at a time independently; the words then follow from
+// one add-with-carry chain lo(P_w) + hi(P_{w-1}) + carry.
 __device__ __forceinline__ void redc(TcShared& sh, TcTile& tt, uint32_t t63, uint32_t (&th)[NW]) {
     const int tile = tt.tile, r = tt.r;
     // ---- GEMM1: m's column sums
@@ -135,20 +168,24 @@ __device__ __forceinline__ void redc(TcShared& sh, TcTile& tt, uint32_t t63, uin
     mbar_wait(tt.mbar, tt.phase);
     tt.phase ^= 1;
     fence_after();
-    uint64_t carry = 0;
-    uint32_t m254 = 0, m255 = 0, m253 = 0;
+    uint32_t hprev = 0;
+    uint32_t m253 = 0, m254 = 0, m255 = 0;
 #pragma unroll
     for (int ch = 0; ch < 8; ch++) {
         uint32_t v[32];
         tmem_ld32(tt.tmem + tt.tlane + 32 * ch, v);
         tmem_ld_wait();
-        uint32_t w[8];
+        uint32_t lo[8], hi[8], w[8];
 #pragma unroll
         for (int q = 0; q < 8; q++) {
-            const uint64_t s = carry + col4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
-            w[q] = (uint32_t)s;
-            carry = s >> 32;
+            const uint64_t p = col4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+            lo[q] = (uint32_t)p;
+            hi[q] = (uint32_t)(p >> 32);
         }
+        w[0] = add_cc(lo[0], hprev);
+#pragma unroll
+        for (int q = 1; q < 8; q++) w[q] = addc_cc(lo[q], hi[q - 1]);
+        hprev = addc(hi[7], 0u);
         *stage_chunk(sh, tile, r, 2 * ch) = make_uint4(w[0], w[1], w[2], w[3]);
         *stage_chunk(sh, tile, r, 2 * ch + 1) = make_uint4(w[4], w[5], w[6], w[7]);
         if (ch == 7) {
@@ -167,52 +204,70 @@ __device__ __forceinline__ void redc(TcShared& sh, TcTile& tt, uint32_t t63, uin
         commit(tt.mbar);
     }
     // columns 508..510 (the top byte products) meanwhile
-    const uint32_t n253 = sh.nw[63] >> 8 & 0xFF, n254 = sh.nw[63] >> 16 & 0xFF, n255 = sh.nw[63] >> 24;
+    const uint32_t n63 = sh.nw[NW - 1];
+    const uint32_t n253 = n63 >> 8 & 0xFF, n254 = n63 >> 16 & 0xFF, n255 = n63 >> 24;
     const uint32_t c508 = m253 * n255 + m254 * n254 + m255 * n253;
     const uint32_t c509 = m254 * n255 + m255 * n254;
     const uint32_t c510 = m255 * n255;
     mbar_wait(tt.mbar, tt.phase);
     tt.phase ^= 1;
     fence_after();
+    // TMEM column idx = global column 252 + idx.  Word w of U (bits 2048 + 32 w)
+    // is P_w over global columns 256 + 4w .. 259 + 4w = idx 4 + 4w .. 7 + 4w.
+    // The carry V out of the low half enters as the "previous high" of word 0.
+    uint32_t carry = 0;
 #pragma unroll
     for (int ch = 0; ch < 8; ch++) {
         uint32_t v[32];
         tmem_ld32(tt.tmem + tt.tlane + 32 * ch, v);
         tmem_ld_wait();
-        // TMEM column idx = global column 252 + idx; word w of U (bits 2048 + 32 w)
-        // covers global columns 256 + 4w .. 259 + 4w = idx 4 + 4w .. 7 + 4w
-        if (ch == 0) {
-            const uint64_t x = (uint64_t)t63 + col4(v[0], v[1], v[2], v[3]);
-            carry = (x + 0xFFFFFFFFull) >> 32;
-        }
+        // words w0 + q, q = 0..7 (chunk 0: q = 0 is the low half's top columns)
+        const int w0 = 8 * ch - 1;
+        uint32_t lo[8], hi[8];
 #pragma unroll
         for (int q = 0; q < 8; q++) {
-            const int w = 8 * ch + q - 1;          // word whose columns start at idx 32 ch + 4 q
-            if (w < 0) continue;
-            const uint64_t s = col4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]) + carry + th[w];
-            th[w] = (uint32_t)s;
-            carry = s >> 32;
+            const uint64_t p = col4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+            lo[q] = (uint32_t)p;
+            hi[q] = (uint32_t)(p >> 32);
         }
+        if (ch == 0) {
+            // V = ceil((T_low's top word + c252 + c253 2^8 + c254 2^16 + c255 2^24) / 2^32)
+            const uint64_t x = (uint64_t)t63 + lo[0] + ((uint64_t)hi[0] << 32);
+            hprev = (uint32_t)((x + 0xFFFFFFFFull) >> 32);
+        }
+        // x_w = lo(P_w) + hi(P_{w-1}) (chain A; the previous chunk's carries
+        // enter with the first word), U_w = th_w + x_w (chain B)
+        const int q0 = (ch == 0) ? 1 : 0;
+        uint32_t x[8];
+        x[q0] = add_cc(lo[q0], hprev + carry);
+#pragma unroll
+        for (int q = q0 + 1; q < 8; q++) x[q] = addc_cc(lo[q], hi[q - 1]);
+        hprev = addc(hi[7], 0u);
+        th[w0 + q0] = add_cc(th[w0 + q0], x[q0]);
+#pragma unroll
+        for (int q = q0 + 1; q < 8; q++) th[w0 + q] = addc_cc(th[w0 + q], x[q]);
+        carry = addc(0u, 0u);
     }
-    // word 63 = columns 508..511 (idx 256..259, past the last chunk)
+    // word 63 = columns 508..511 (idx 256..259, past the last chunk), then bit 2048
     {
-        const uint64_t s = col4(c508, c509, c510, 0) + carry + th[NW - 1];
-        th[NW - 1] = (uint32_t)s;
-        carry = s >> 32;
+        const uint64_t p = col4(c508, c509, c510, 0) + hprev + carry;
+        th[NW - 1] = add_cc(th[NW - 1], (uint32_t)p);
+        carry = addc(0u, (uint32_t)(p >> 32));
     }
-    // U < 2n: subtract n once if U >= n (U's bit 2048 is `carry`): the borrow
-    // chain of U - n decides, then the subtraction runs under a mask
-    uint32_t borrow = 0;
+    // U < 2n: subtract n once if U >= n (U's bit 2048 is `carry`).  The top
+    // words decide unless they are equal (probability ~2^-32): then the full
+    // borrow chain of U - n does.
+    bool ge = carry != 0 || th[NW - 1] > n63;
+    if (carry == 0 && th[NW - 1] == n63) {
+        uint32_t borrow = 0;
 #pragma unroll
-    for (int w = 0; w < NW; w++) borrow = (uint32_t)(((uint64_t)th[w] - sh.nw[w] - borrow) >> 32) & 1;
-    const uint32_t mask = (carry != 0 || borrow == 0) ? 0xFFFFFFFFu : 0u;
-    borrow = 0;
-#pragma unroll
-    for (int w = 0; w < NW; w++) {
-        const uint64_t s = (uint64_t)th[w] - (sh.nw[w] & mask) - borrow;
-        th[w] = (uint32_t)s;
-        borrow = (uint32_t)(s >> 32) & 1;
+        for (int w = 0; w < NW; w++) borrow = (uint32_t)(((uint64_t)th[w] - sh.nw[w] - borrow) >> 32) & 1;
+        ge = borrow == 0;
     }
+    const uint32_t mask = ge ? 0xFFFFFFFFu : 0u;
+    th[0] = sub_cc(th[0], sh.nw[0] & mask);
+#pragma unroll
+    for (int w = 1; w < NW; w++) th[w] = subc_cc(th[w], sh.nw[w] & mask);
 }
 
 }  // namespace tc

@@ -61,6 +61,55 @@ __host__ __device__ __forceinline__ void mul_scan(const double (&a)[ND], BF b, P
     }
 }
 
+// T = A B by rows (operand scanning), the loop NOT unrolled (~40 products of
+// code instead of mul_scan's ND^2): iteration j adds a_i b_j to ND running
+// 64-bit columns (low half to column j+i, high half to j+i+1), emits the
+// completed column j through lowout(j, digit), and shifts the columns down
+// by one in place (t[i-1] = t[i] + ...: CIOS's rename without the q n row).
+// lowout may overwrite b's digit j (b(j) is read one iteration ahead).  After
+// the loop the low digits are replayed into put in order (lowin(k) returns
+// what lowout(k) stored), then the high columns are normalised into put.
+// Column bounds: <= 2 terms < 2^52 per column per iteration, <= ND iterations.
+template <int ND, typename BF, typename LO, typename LI, typename Put>
+__host__ __device__ __forceinline__ void mul_rows(const double (&a)[ND], BF b, LO lowout, LI lowin, Put put) {
+    uint64_t t[ND];
+#pragma unroll
+    for (int i = 0; i < ND; i++) t[i] = 0;
+    uint64_t bias = BL, carry = 0;
+    double bj = b(0);
+#ifdef __CUDA_ARCH__
+#pragma unroll 1
+#endif
+    for (int j = 0; j < ND; j++) {
+        const double bn = b(j + 1 < ND ? j + 1 : j);
+        const double h0 = fma_rz(a[0], bj, C104);
+        const double l0 = fma_rz(a[0], bj, sub_rn(C2, h0));
+        const uint64_t v = t[0] + bits(l0) - bias + carry;   // column j: (j+1) lows, j highs
+        carry = v >> D;
+        lowout(j, v & M52);
+        uint64_t hp = bits(h0);
+#pragma unroll
+        for (int i = 1; i < ND; i++) {
+            const double h = fma_rz(a[i], bj, C104);
+            const double l = fma_rz(a[i], bj, sub_rn(C2, h));
+            t[i - 1] = t[i] + bits(l) + hp;
+            hp = bits(h);
+        }
+        t[ND - 1] = hp;
+        bias += BL + BH;
+        bj = bn;
+    }
+#pragma unroll
+    for (int k = 0; k < ND; k++) put(k, lowin(k));
+    // t[p] = column ND + p: (ND-1-p) lows, (ND-p) highs
+#pragma unroll
+    for (int p = 0; p < ND; p++) {
+        const uint64_t v = t[p] - ((uint64_t)(ND - 1 - p) * BL + (uint64_t)(ND - p) * BH) + carry;
+        carry = v >> D;
+        put(ND + p, v & M52);
+    }
+}
+
 // digit stream -> 32-bit words (words 0 .. NWORDS-1; bits beyond are dropped).
 // put(k, d) must be called for k = 0, 1, 2, ... in order.
 template <int NWORDS, typename Word>
