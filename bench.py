@@ -35,6 +35,13 @@ import workload  # noqa: E402
 METRIC = "RSA-2048 modexps/sec (e=65537 and full d) at 1/2/4/8 B200; % of IMAD peak"
 R_PRODUCTS_PER_CLK_PER_SM = 32      # measured: profiles/r01_imad_peak.jsonl (IMAD.WIDE half rate)
 DFMA_PER_CLK_PER_SM = 64            # nominal FP64 pipe (ncu); fma.rn.f64 microbenchmark sustains 53.6
+LANE_OPS_PER_CLK_PER_SM = 64        # 16-lane pipes (FP64, INT32 ALU, IMAD) share issue: 4 SMSPs x 16 lanes
+                                    # per clock (profiles/r02_dfma_mix.jsonl: each such instruction costs
+                                    # 2 SMSP cycles whichever of them it is; only FP32 co-issues)
+TC_MMA_MACS_PER_OP = 114688         # u8 MACs per packet per Montgomery op on the tensor core (S = 64):
+                                    # GEMM1 12 MMAs x (128 x 128 x 32) + GEMM2 8 x (128 x 256 x 32), / 128 packets
+TC_GEMM_WORDS_PER_OP = 128          # 32-bit words assembled from the two GEMMs' byte columns per op
+
 
 WORKLOADS = {
     # name: (key, count, legs)   legs: list of (label, exponent field, input)
@@ -69,7 +76,7 @@ def parse():
                     help="process-group backend for N > 1 (gloo: test the multi-rank path on fewer GPUs)")
     ap.add_argument("--kernel-path", action="append", default=[], metavar="S=PATH",
                     help="A/B only: run width class S on another kernel (rsa_set_kernel_path), PATH one of "
-                         "fp64, int, int_group, int_pair, int_multi; e.g. --kernel-path 64=int")
+                         "tc, fp64, int, int_group, int_pair, int_multi; e.g. --kernel-path 64=fp64")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=20.0, help="CPU-seconds budget of the oracle sample")
@@ -255,6 +262,8 @@ def batch_kernel_name(R, S: int) -> str:
     path = R.rsa_get_kernel_path(S)
     if path == R.RSA_PATH_FP64:
         return f"modexp_f64_kernel<{S}>"
+    if path == R.RSA_PATH_TC:
+        return "modexp_tc_kernel"
     if path == R.RSA_PATH_INT_MULTI:
         return f"modexp_small_kernel<{S}>"
     if path == R.RSA_PATH_INT_GROUP:
@@ -521,7 +530,8 @@ def run_ours(args, rank, world, local_rank):
     products = count * plans[dom]["products"]
     achieved = products / (leg_ms[dom] / 1e3) / 1e12
     peak = R_PRODUCTS_PER_CLK_PER_SM * sms * f_max * 1e6 / 1e12
-    fp64 = kind in ("batch", "crt") and plans[dom].get("fp64_digits", 0) > 0
+    fp64 = kind in ("batch", "crt") and plans[dom].get("fp64_digits", 0) > 0 and \
+        not (kind == "batch" and batch_kernel_name(R, S) == "modexp_tc_kernel")
     roofline = {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "Tprod/s", "frac": achieved / peak,
                 "traffic": ncu_traffic(key_name, legs[dom][0], count),
                 "traffic_unit": "bytes per launch", "algorithmic_bytes": count * s * 4 * 2,
@@ -569,13 +579,45 @@ def run_ours(args, rank, world, local_rank):
                            "peak_source": "nominal (half-rate IMAD.WIDE, profiles/r01_imad_peak.jsonl)",
                            "basis": "the path's 32x32->64 limb-product count (the metric's '% of IMAD peak') "
                                     "against 32 products/clk/SM on the integer pipe"}})
+    tc = kind == "batch" and batch_kernel_name(R, S) == "modexp_tc_kernel"
+    if tc:
+        # Tensor-core reduction kernel (modexp_tc.cu): the CUDA cores' 16-lane
+        # issue (FP64 + INT32 share it) is the bound.  Algorithmic lane-ops per
+        # packet: 5 per 52x52 digit product of T = A B (3 FP64 for the exact
+        # split + the 64-bit column add, the representation's floor:
+        # r02_dfma_mix) and 4 per word assembled from the GEMMs' byte columns
+        # (3 IMAD.WIDE + 1 add-with-carry).  The tensor core's own share is
+        # reported beside it against the int8 peak.
+        pd = plans[dom]
+        lane_ops = 5 * pd["digit_products"] + 4 * TC_GEMM_WORDS_PER_OP * pd["montmuls"]
+        l_ach = count * lane_ops / (leg_ms[dom] / 1e3) / 1e12
+        l_peak = LANE_OPS_PER_CLK_PER_SM * sms * f_max * 1e6 / 1e12
+        i8_peak = 2 * float(peaks.get("bf16_tflops_sustained", 1378.2))      # int8 = 2 x bf16 (guide's ratio)
+        i8_ach = count * 2 * TC_MMA_MACS_PER_OP * pd["montmuls"] / (leg_ms[dom] / 1e3) / 1e12
+        roofline.update({
+            "bound": "alu", "achieved": l_ach, "peak": l_peak, "unit": "T lane-op/s", "frac": l_ach / l_peak,
+            "algorithmic": f"{lane_ops} CUDA-core lane-ops/packet: {pd['digit_products']} 52x52 digit products "
+                           f"x 5 (T = A B; {pd['squarings']} squarings x ND(ND+1)/2 + "
+                           f"{pd['montmuls'] - pd['squarings']} multiplies x ND^2, ND={pd['fp64_digits']}) + "
+                           f"{pd['montmuls']} ops x {TC_GEMM_WORDS_PER_OP} GEMM output words x 4, x {count} packets",
+            "peak_basis": f"{LANE_OPS_PER_CLK_PER_SM} lane-ops/clk/SM (4 SMSPs x 16 lanes of the FP64 / INT32 "
+                          f"pipes, one shared issue) x {sms} SMs x {f_max:.0f} MHz (MEASURED_PEAKS sm_max_mhz)",
+            "peak_source": "nominal: MEASURED_PEAKS.json has no FP64/INT32 entry; frac is 'of nominal'",
+            "tensor": {"achieved": i8_ach, "peak": i8_peak, "unit": "T int8-op/s", "frac": i8_ach / i8_peak,
+                       "algorithmic": f"{TC_MMA_MACS_PER_OP} u8 MACs x 2 per packet per Montgomery op "
+                                      f"(m = T n' mod R, columns of m n) x {pd['montmuls']} ops",
+                       "peak_source": "2 x MEASURED_PEAKS bf16_tflops_sustained (guide: int8/fp8 = 2 x bf16 dense)"},
+            "imad_equiv": {"achieved": achieved, "peak": peak, "unit": "Tprod/s", "frac": achieved / peak,
+                           "peak_source": "nominal (half-rate IMAD.WIDE, profiles/r01_imad_peak.jsonl)",
+                           "basis": "the metric's '% of IMAD peak': the textbook 32x32->64 limb-product count "
+                                    "of the same Montgomery ops against 32 products/clk/SM on the integer pipe"}})
     if kind == "batch":
         # the window table is algorithmic state too: every entry written once,
         # read by each window multiply (+ the A loads); per resident thread it is
         # ntab x S limbs, larger than L2 at S = 64 / w = 7, so it streams to DRAM
         pd = plans[dom]
         touches = pd["table_entries"] + (pd["montmuls"] - pd["squarings"] - 2) + 2
-        entry = 8 * pd["fp64_digits"] if fp64 else S * 4        # 52-bit digits as doubles, or limbs
+        entry = 8 * pd["fp64_digits"] if (fp64 or tc) else S * 4   # 52-bit digits as doubles, or limbs
         roofline["algorithmic_table_bytes"] = count * entry * touches
         roofline["traffic_note"] = ("DRAM traffic = packet I/O + the per-thread sliding-window table "
                                     f"({pd['table_entries']} entries x {entry} B, {touches} entry reads/writes per "
@@ -599,7 +641,7 @@ def run_ours(args, rank, world, local_rank):
         cpu = cpu_baseline(key, base_np, legs, args.cpu_seconds)
     line = {"metric": METRIC, "value": value, "unit": "modexp/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "strong",
-            "vs_baseline": None, "dtype": "f64" if fp64 else "u32", "data": "synthetic",
+            "vs_baseline": None, "dtype": "f64+u8" if tc else ("f64" if fp64 else "u32"), "data": "synthetic",
             "config": {"workload": args.config, "packets_total": total, "packets_per_rank": per,
                        **({"kernel_path": args.kernel_path} if args.kernel_path else {}),
                        "key": key_name + " (seeded, "

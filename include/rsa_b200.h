@@ -241,7 +241,7 @@ int rsa_set_window(int w);
  * thread shape differ.  Paths:
  *   RSA_PATH_DEFAULT    the measured default of the class (see below)
  *   RSA_PATH_FP64       S = 32, 64, 128: 52-bit digits on the FP64 pipe
- *                       (default for those classes)
+ *                       (default for S = 32, 128)
  *   RSA_PATH_INT        32-bit limbs, IMAD carry chains, one thread per packet
  *                       (default for S = 8, 16; for S = 128 it means the
  *                       2-lane pair kernel)
@@ -252,10 +252,11 @@ int rsa_set_window(int w);
  *                       Montgomery reduction (m = T n' mod R, T + m n) as u8
  *                       matrix products on the tensor core (tcgen05, TMEM),
  *                       R = 2^2048; 128-packet tiles, one CTA per SM
+ *                       (default for S = 64)
  * rsa_set_kernel_path sets the path of class `width_class` for subsequent
  * calls of every thread (process-wide, thread-safe; a call in flight keeps the
  * path it started with).  RSA_PATH_DEFAULT restores the default, under which
- * the RSA_B200_F64 / _F64_4096 / _SHAPE64 / _TPI128 / _SMALL environment
+ * the RSA_B200_F64 / _F64_4096 / _TC / _SHAPE64 / _TPI128 / _SMALL environment
  * switches of the A/B tools are honoured (read per call).
  * Errors: RSA_EINVAL (no such class, or the class has no such kernel).
  * rsa_get_kernel_path returns the path the class resolves to now (never

@@ -810,7 +810,7 @@ int rsa_b200_resolve_path(int S) {
         else if (S == 64)
             p = env_is("RSA_B200_SHAPE64", 'g') ? RSA_PATH_INT_GROUP
                 : env_is("RSA_B200_F64", '0')   ? RSA_PATH_INT
-                : env_is("RSA_B200_TC", '1')    ? RSA_PATH_TC : RSA_PATH_FP64;
+                : env_is("RSA_B200_TC", '0')    ? RSA_PATH_FP64 : RSA_PATH_TC;
         else
             p = (env_is("RSA_B200_F64", '0') || env_is("RSA_B200_F64_4096", '0'))
                     ? (env_is("RSA_B200_TPI128", '4') ? RSA_PATH_INT_GROUP : RSA_PATH_INT_PAIR)

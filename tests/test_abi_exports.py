@@ -103,10 +103,11 @@ def test_kernel_path_knob():
     import paper_1407_1465_b200 as R
     import workload
     defaults = {2: R.RSA_PATH_INT_MULTI, 4: R.RSA_PATH_INT_MULTI, 8: R.RSA_PATH_INT, 16: R.RSA_PATH_INT,
-                32: R.RSA_PATH_FP64, 64: R.RSA_PATH_FP64, 128: R.RSA_PATH_FP64}
+                32: R.RSA_PATH_FP64, 64: R.RSA_PATH_TC, 128: R.RSA_PATH_FP64}
     for S, p in defaults.items():
         assert R.rsa_get_kernel_path(S) == p, S
-    for S, p in [(8, R.RSA_PATH_FP64), (64, R.RSA_PATH_INT_PAIR), (128, R.RSA_PATH_INT_MULTI), (3, 0), (64, 9)]:
+    for S, p in [(8, R.RSA_PATH_FP64), (64, R.RSA_PATH_INT_PAIR), (128, R.RSA_PATH_INT_MULTI), (3, 0), (64, 9),
+                 (32, R.RSA_PATH_TC), (128, R.RSA_PATH_TC)]:
         with pytest.raises(R.RsaError):
             R.rsa_set_kernel_path(S, p)
     with pytest.raises(R.RsaError):
@@ -118,8 +119,15 @@ def test_kernel_path_knob():
         assert R.rsa_get_kernel_path(64) == R.RSA_PATH_INT_GROUP
     with R.kernel_path(128, R.RSA_PATH_INT):           # S = 128 integer = the lane pairs
         assert R.rsa_get_kernel_path(128) == R.RSA_PATH_INT_PAIR
-    assert R.rsa_get_kernel_path(64) == R.RSA_PATH_FP64
-    assert fp["fp64_digits"] == 40 and fp["sqr_kernel"] == 1
+    with R.kernel_path(64, R.RSA_PATH_FP64):
+        f64 = R.rsa_plan_info(k["d"], k["n"], 2048)
+    assert R.rsa_get_kernel_path(64) == R.RSA_PATH_TC
+    assert fp["fp64_digits"] == 40 and fp["sqr_kernel"] == 1 and f64["fp64_digits"] == 40
+    # the tensor-core path's CUDA-core digit products: the product T = A B only
+    # (ND(ND+1)/2 per squaring, ND^2 per multiply); the FP64 kernel adds ND^2 of reduction
+    nsq, nmul = fp["squarings"], fp["montmuls"] - fp["squarings"]
+    assert fp["digit_products"] == nsq * 820 + nmul * 1600
+    assert f64["digit_products"] == nsq * (820 + 1600) + nmul * 3200
     assert grp["fp64_digits"] == 0 and grp["sqr_kernel"] == 0
     assert grp["products"] > fp["products"]          # no dedicated squaring on the group kernel
     assert R.rsa_plan_info(k["d"], k["n"], 2048) == fp

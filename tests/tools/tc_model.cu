@@ -1,0 +1,82 @@
+// tc_model.cu -- host build of the CUDA-core half of the tensor-core
+// Montgomery multiply (paper_1407_1465_b200/csrc/tc_digits.cuh, and
+// f64::sqr_scan from mont_f64.cuh) for tests/test_tc_model.py.  Compiled with
+// nvcc for the host; the rounding mode is set toward zero (the DFMA.RZ split).
+// Protocol (one line per command, hex numbers, stdout one hex line):
+//   M a b   T = A B through mul_rows + Packer (128 words)
+//   Q a     T = A^2 through sqr_scan + Packer
+//   C a b   T = A B through mul_scan + Packer
+//   W x     x (64 words) -> 40 digits (words_to_digits) -> back to words (Packer)
+#include <cfenv>
+#include <cstdint>
+#include <cstdio>
+#include <cstring>
+#include <iostream>
+#include <sstream>
+#include <string>
+
+#include "../../paper_1407_1465_b200/csrc/tc_digits.cuh"
+
+using namespace rsa_b200;
+constexpr int ND = 40, NW = 64;
+
+static void parse_words(const std::string& hex, uint32_t* w, int n) {
+    for (int i = 0; i < n; i++) w[i] = 0;
+    int bit = 0;
+    for (int i = (int)hex.size() - 1; i >= 0 && bit < 32 * n; i--, bit += 4) {
+        const char c = hex[i];
+        const uint32_t v = (c >= '0' && c <= '9') ? c - '0' : (c >= 'a' && c <= 'f') ? c - 'a' + 10 : c - 'A' + 10;
+        w[bit / 32] |= v << (bit % 32);
+    }
+}
+
+static void print_words(const uint32_t* w, int n) {
+    int top = n - 1;
+    while (top > 0 && w[top] == 0) top--;
+    printf("%x", w[top]);
+    for (int i = top - 1; i >= 0; i--) printf("%08x", w[i]);
+    printf("\n");
+    fflush(stdout);
+}
+
+int main() {
+    fesetround(FE_TOWARDZERO);
+    std::string line;
+    while (std::getline(std::cin, line)) {
+        std::istringstream is(line);
+        std::string op, x, y;
+        is >> op >> x >> y;
+        uint32_t aw[NW], bw[NW], out[2 * NW];
+        parse_words(x, aw, NW);
+        parse_words(y.empty() ? "0" : y, bw, NW);
+        double a[ND], b[ND];
+        tcd::words_to_digits<ND>([&](int w) -> uint32_t { return w < NW ? aw[w] : 0u; }, a);
+        tcd::words_to_digits<ND>([&](int w) -> uint32_t { return w < NW ? bw[w] : 0u; }, b);
+        memset(out, 0, sizeof(out));
+        auto word = [&](int w, uint32_t v) { out[w] = v; };
+        tcd::Packer<2 * NW, decltype(word)> pk{word, 0};
+        auto put = [&](int k, uint64_t d) { pk.put(k, d); };
+        if (op == "M") {
+            uint64_t low[ND];
+            double bs[ND];
+            memcpy(bs, b, sizeof(b));
+            tcd::mul_rows<ND>(
+                a, [&](int j) { return bs[j]; },
+                [&](int j, uint64_t d) { memcpy(&bs[j], &d, 8); low[j] = d; },   // overwrites b_j, like the kernel
+                [&](int j) { return low[j]; }, put);
+        } else if (op == "Q") {
+            f64::sqr_scan<ND>(a, put);
+        } else if (op == "C") {
+            tcd::mul_scan<ND>(a, [&](int j) { return b[j]; }, put);
+        } else if (op == "W") {
+            for (int k = 0; k < ND; k++) put(k, (uint64_t)a[k]);
+            for (int k = ND; k < 2 * ND; k++) put(k, 0);
+        } else {
+            printf("?\n");
+            fflush(stdout);
+            continue;
+        }
+        print_words(out, 2 * NW);
+    }
+    return 0;
+}
