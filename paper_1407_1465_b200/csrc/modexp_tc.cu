@@ -33,6 +33,11 @@
 
 namespace rsa_b200 {
 
+#ifndef RSA_TC_LOCK
+#define RSA_TC_LOCK 1   // both tiles start every op together (A/B: 900.5K vs 809K: the unrolled squaring is
+                        // ~85 KB of SASS and two tiles on different code lines stall on instruction fetch)
+#endif
+
 constexpr int TC_S = 64;
 constexpr int TC_ND = rsa_f64_digits(TC_S);    // 40 digits of 52 bits (A < n < 2^2048)
 constexpr int TC_BLOCK = 256;
@@ -130,6 +135,7 @@ __global__ void __launch_bounds__(TC_BLOCK, 1) modexp_tc_kernel(const __grid_con
                 for (int k = 0; k < ND; k++) bslot[k * TC_BLOCK] = (k == 0) ? 1.0 : 0.0;
             }
             for (int r = 0; r < op.rep; r++) {
+                if constexpr (RSA_TC_LOCK != 0) __syncthreads();   // A/B: both tiles on the same code lines
                 // T = A B: words 0..63 to the staging buffer (16-byte chunks), 64..127 to th
                 uint32_t t63 = 0, wb0 = 0, wb1 = 0, wb2 = 0;
                 auto word = [&](int w, uint32_t v) {
