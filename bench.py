@@ -273,14 +273,16 @@ def batch_kernel_name(R, S: int) -> str:
     return f"modexp_kernel<{S}>"
 
 
-def ncu_traffic(key_name: str, leg: str, count: int):
+def ncu_traffic(key_name: str, leg: str, count: int, kernel_tag: str = ""):
     """DRAM bytes (read + write) per launch of the dominant kernel, from the
     committed ncu --set full capture (profiles/ncu_traffic.json, bytes per
-    packet) scaled to this launch's packets; None if not captured."""
+    packet; entry `leg + kernel_tag` when the kernel has its own capture)
+    scaled to this launch's packets; None if not captured."""
     path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     try:
         with open(path) as f:
-            rec = json.load(f).get(key_name, {}).get(leg)
+            recs = json.load(f).get(key_name, {})
+            rec = recs.get(leg + kernel_tag) or recs.get(leg)
     except (OSError, ValueError):
         return None
     return None if not rec else rec["bytes_per_packet"] * count
@@ -533,7 +535,9 @@ def run_ours(args, rank, world, local_rank):
     fp64 = kind in ("batch", "crt") and plans[dom].get("fp64_digits", 0) > 0 and \
         not (kind == "batch" and batch_kernel_name(R, S) == "modexp_tc_kernel")
     roofline = {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "Tprod/s", "frac": achieved / peak,
-                "traffic": ncu_traffic(key_name, legs[dom][0], count),
+                "traffic": ncu_traffic(key_name, legs[dom][0], count,
+                                       "_tc" if kind == "batch" and batch_kernel_name(R, S) == "modexp_tc_kernel"
+                                       else ""),
                 "traffic_unit": "bytes per launch", "algorithmic_bytes": count * s * 4 * 2,
                 "kernel": ({"multi": f"modexp_multi_kernel<{S}>", "mr": f"modexp_multi_kernel<{S}> (MR mode)",
                             "crt": f"2 x {batch_kernel_name(R, S)} + crt_split/combine (half-width CRT legs; "
