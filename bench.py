@@ -38,9 +38,18 @@ DFMA_PER_CLK_PER_SM = 64            # nominal FP64 pipe (ncu); fma.rn.f64 microb
 LANE_OPS_PER_CLK_PER_SM = 64        # 16-lane pipes (FP64, INT32 ALU, IMAD) share issue: 4 SMSPs x 16 lanes
                                     # per clock (profiles/r02_dfma_mix.jsonl: each such instruction costs
                                     # 2 SMSP cycles whichever of them it is; only FP32 co-issues)
-TC_MMA_MACS_PER_OP = 114688         # u8 MACs per packet per Montgomery op on the tensor core (S = 64):
-                                    # GEMM1 12 MMAs x (128 x 128 x 32) + GEMM2 8 x (128 x 256 x 32), / 128 packets
-TC_GEMM_WORDS_PER_OP = 128          # 32-bit words assembled from the two GEMMs' byte columns per op
+
+
+def tc_macs_per_op(S: int) -> int:
+    """u8 MACs per packet per Montgomery op on the tensor core (mont_tc.cuh, KB = 4S
+    bytes): GEMM1 = N = 128 blocks b with 4b + 4 K-blocks of 32, GEMM2 = KB x KB."""
+    kb = 4 * S
+    return sum((4 * b + 4) * 32 * 128 for b in range(kb // 128)) + kb * kb   # 114688 at S = 64
+
+
+def tc_words_per_op(S: int) -> int:
+    """32-bit words assembled from the two GEMMs' byte columns per op (2 x S)."""
+    return 2 * S
 
 
 WORKLOADS = {
@@ -282,7 +291,7 @@ def ncu_traffic(key_name: str, leg: str, count: int, kernel_tag: str = ""):
     try:
         with open(path) as f:
             recs = json.load(f).get(key_name, {})
-            rec = recs.get(leg + kernel_tag) or recs.get(leg)
+            rec = recs.get(leg + kernel_tag)     # a kernel without its own capture: None
     except (OSError, ValueError):
         return None
     return None if not rec else rec["bytes_per_packet"] * count
@@ -533,10 +542,10 @@ def run_ours(args, rank, world, local_rank):
     achieved = products / (leg_ms[dom] / 1e3) / 1e12
     peak = R_PRODUCTS_PER_CLK_PER_SM * sms * f_max * 1e6 / 1e12
     fp64 = kind in ("batch", "crt") and plans[dom].get("fp64_digits", 0) > 0 and \
-        not (kind == "batch" and batch_kernel_name(R, S) == "modexp_tc_kernel")
+        batch_kernel_name(R, S) != "modexp_tc_kernel"
     roofline = {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "Tprod/s", "frac": achieved / peak,
                 "traffic": ncu_traffic(key_name, legs[dom][0], count,
-                                       "_tc" if kind == "batch" and batch_kernel_name(R, S) == "modexp_tc_kernel"
+                                       "_tc" if kind in ("batch", "crt") and batch_kernel_name(R, S) == "modexp_tc_kernel"
                                        else ""),
                 "traffic_unit": "bytes per launch", "algorithmic_bytes": count * s * 4 * 2,
                 "kernel": ({"multi": f"modexp_multi_kernel<{S}>", "mr": f"modexp_multi_kernel<{S}> (MR mode)",
@@ -583,7 +592,7 @@ def run_ours(args, rank, world, local_rank):
                            "peak_source": "nominal (half-rate IMAD.WIDE, profiles/r01_imad_peak.jsonl)",
                            "basis": "the path's 32x32->64 limb-product count (the metric's '% of IMAD peak') "
                                     "against 32 products/clk/SM on the integer pipe"}})
-    tc = kind == "batch" and batch_kernel_name(R, S) == "modexp_tc_kernel"
+    tc = kind in ("batch", "crt") and batch_kernel_name(R, S) == "modexp_tc_kernel"
     if tc:
         # Tensor-core reduction kernel (modexp_tc.cu): the CUDA cores' 16-lane
         # issue (FP64 + INT32 share it) is the bound.  Algorithmic lane-ops per
@@ -593,22 +602,23 @@ def run_ours(args, rank, world, local_rank):
         # (3 IMAD.WIDE + 1 add-with-carry).  The tensor core's own share is
         # reported beside it against the int8 peak.
         pd = plans[dom]
-        lane_ops = 5 * pd["digit_products"] + 4 * TC_GEMM_WORDS_PER_OP * pd["montmuls"]
+        lane_ops = 5 * pd["digit_products"] + 4 * tc_words_per_op(S) * pd["montmuls"]
         l_ach = count * lane_ops / (leg_ms[dom] / 1e3) / 1e12
         l_peak = LANE_OPS_PER_CLK_PER_SM * sms * f_max * 1e6 / 1e12
         i8_peak = 2 * float(peaks.get("bf16_tflops_sustained", 1378.2))      # int8 = 2 x bf16 (guide's ratio)
-        i8_ach = count * 2 * TC_MMA_MACS_PER_OP * pd["montmuls"] / (leg_ms[dom] / 1e3) / 1e12
+        i8_ach = count * 2 * tc_macs_per_op(S) * pd["montmuls"] / (leg_ms[dom] / 1e3) / 1e12
         roofline.update({
             "bound": "alu", "achieved": l_ach, "peak": l_peak, "unit": "T lane-op/s", "frac": l_ach / l_peak,
             "algorithmic": f"{lane_ops} CUDA-core lane-ops/packet: {pd['digit_products']} 52x52 digit products "
                            f"x 5 (T = A B; {pd['squarings']} squarings x ND(ND+1)/2 + "
                            f"{pd['montmuls'] - pd['squarings']} multiplies x ND^2, ND={pd['fp64_digits']}) + "
-                           f"{pd['montmuls']} ops x {TC_GEMM_WORDS_PER_OP} GEMM output words x 4, x {count} packets",
+                           f"{pd['montmuls']} ops x {tc_words_per_op(S)} GEMM output words x 4, x {count} packets"
+                           + (" (both CRT halves)" if kind == "crt" else ""),
             "peak_basis": f"{LANE_OPS_PER_CLK_PER_SM} lane-ops/clk/SM (4 SMSPs x 16 lanes of the FP64 / INT32 "
                           f"pipes, one shared issue) x {sms} SMs x {f_max:.0f} MHz (MEASURED_PEAKS sm_max_mhz)",
             "peak_source": "nominal: MEASURED_PEAKS.json has no FP64/INT32 entry; frac is 'of nominal'",
             "tensor": {"achieved": i8_ach, "peak": i8_peak, "unit": "T int8-op/s", "frac": i8_ach / i8_peak,
-                       "algorithmic": f"{TC_MMA_MACS_PER_OP} u8 MACs x 2 per packet per Montgomery op "
+                       "algorithmic": f"{tc_macs_per_op(S)} u8 MACs x 2 per packet per Montgomery op "
                                       f"(m = T n' mod R, columns of m n) x {pd['montmuls']} ops",
                        "peak_source": "2 x MEASURED_PEAKS bf16_tflops_sustained (guide: int8/fp8 = 2 x bf16 dense)"},
             "imad_equiv": {"achieved": achieved, "peak": peak, "unit": "Tprod/s", "frac": achieved / peak,

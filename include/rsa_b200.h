@@ -241,18 +241,18 @@ int rsa_set_window(int w);
  * thread shape differ.  Paths:
  *   RSA_PATH_DEFAULT    the measured default of the class (see below)
  *   RSA_PATH_FP64       S = 32, 64, 128: 52-bit digits on the FP64 pipe
- *                       (default for S = 32, 128)
+ *                       (default for S = 128)
  *   RSA_PATH_INT        32-bit limbs, IMAD carry chains, one thread per packet
  *                       (default for S = 8, 16; for S = 128 it means the
  *                       2-lane pair kernel)
  *   RSA_PATH_INT_GROUP  S = 64: 2 lanes per packet; S = 128: 4 lanes
  *   RSA_PATH_INT_PAIR   S = 128: 2 lanes per packet
  *   RSA_PATH_INT_MULTI  S = 2, 4: several packets per thread (default there)
- *   RSA_PATH_TC         S = 64: the product A B on the FP64 pipe, the
+ *   RSA_PATH_TC         S = 32, 64: the product A B on the FP64 pipe, the
  *                       Montgomery reduction (m = T n' mod R, T + m n) as u8
  *                       matrix products on the tensor core (tcgen05, TMEM),
- *                       R = 2^2048; 128-packet tiles, one CTA per SM
- *                       (default for S = 64)
+ *                       R = 2^(32 S); 128-packet tiles, one CTA per SM
+ *                       (default for S = 32, 64)
  * rsa_set_kernel_path sets the path of class `width_class` for subsequent
  * calls of every thread (process-wide, thread-safe; a call in flight keeps the
  * path it started with).  RSA_PATH_DEFAULT restores the default, under which

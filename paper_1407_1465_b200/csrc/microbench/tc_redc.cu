@@ -17,7 +17,9 @@ __global__ void __launch_bounds__(256, 1)
 tc_redc_test(const uint32_t* __restrict__ T, uint32_t* __restrict__ U, uint32_t* __restrict__ M,
              const uint8_t* __restrict__ npb, const uint8_t* __restrict__ nb, int reps) {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
-    TcShared& sh = *reinterpret_cast<TcShared*>(smem_raw);
+    using Sh = TcShared<256, 2>;
+    constexpr int NW = Geom<256>::NW;
+    Sh& sh = *reinterpret_cast<Sh*>(smem_raw);
     const int warp = threadIdx.x / 32;
     if (warp == 0) tmem_alloc(smem_u32(&sh.tmem_base), 512);
     if (threadIdx.x == 0) {
@@ -105,7 +107,7 @@ int main(int argc, char** argv) {
     CK(cudaMemcpy(dT, T.data(), T.size() * 4, cudaMemcpyHostToDevice));
     CK(cudaMemcpy(dn, n.data(), 256, cudaMemcpyHostToDevice));
     CK(cudaMemcpy(dnp, np.data(), 256, cudaMemcpyHostToDevice));
-    const int smem = sizeof(TcShared) + 1024;
+    const int smem = sizeof(TcShared<256, 2>) + 1024;
     CK(cudaFuncSetAttribute(tc_redc_test, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     tc_redc_test<<<count / 256, 256, smem>>>(dT, dU, dM, dnp, dn, 1);
     CK(cudaGetLastError());

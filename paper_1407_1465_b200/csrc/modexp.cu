@@ -784,7 +784,7 @@ int rsa_b200_path_valid(int S, int path) {
     case RSA_PATH_INT_GROUP: return S == 64 || S == 128;
     case RSA_PATH_INT_PAIR: return S == 128;
     case RSA_PATH_INT_MULTI: return S <= 4;
-    case RSA_PATH_TC: return S == 64;
+    case RSA_PATH_TC: return S == 32 || S == 64;
     default: return 0;
     }
 }
@@ -806,7 +806,8 @@ int rsa_b200_resolve_path(int S) {
     if (p == RSA_PATH_DEFAULT) {
         if (S <= 4) p = env_is("RSA_B200_SMALL", '0') ? RSA_PATH_INT : RSA_PATH_INT_MULTI;
         else if (S <= 16) p = RSA_PATH_INT;
-        else if (S == 32) p = env_is("RSA_B200_F64", '0') ? RSA_PATH_INT : RSA_PATH_FP64;
+        else if (S == 32)
+            p = env_is("RSA_B200_F64", '0') ? RSA_PATH_INT : env_is("RSA_B200_TC", '0') ? RSA_PATH_FP64 : RSA_PATH_TC;
         else if (S == 64)
             p = env_is("RSA_B200_SHAPE64", 'g') ? RSA_PATH_INT_GROUP
                 : env_is("RSA_B200_F64", '0')   ? RSA_PATH_INT

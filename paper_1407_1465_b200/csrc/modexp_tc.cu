@@ -33,28 +33,47 @@
 
 namespace rsa_b200 {
 
+#ifndef RSA_TC_TILES32
+#define RSA_TC_TILES32 4    // 1024-bit class: tiles of 128 packets per CTA (TMEM 128 columns each)
+#endif
+#ifndef RSA_TC_SQREC32
+#define RSA_TC_SQREC32 1
+#endif
+#ifndef RSA_TC_SQREC64
+#define RSA_TC_SQREC64 0
+#endif
 #ifndef RSA_TC_LOCK
 #define RSA_TC_LOCK 1   // both tiles start every op together (A/B: 900.5K vs 809K: the unrolled squaring is
                         // ~85 KB of SASS and two tiles on different code lines stall on instruction fetch)
 #endif
 
-constexpr int TC_S = 64;
-constexpr int TC_ND = rsa_f64_digits(TC_S);    // 40 digits of 52 bits (A < n < 2^2048)
-constexpr int TC_BLOCK = 256;
-static_assert(TC_ND == 40, "2048-bit class");
+// Class S (32-bit limbs): KB = 4 S bytes per operand, ND digits of 52 bits
+// (A < n < 2^(32 S)), TILES tiles of 128 packets per CTA (TMEM: KB columns each).
+template <int S>
+struct TcCfg {
+    static constexpr int KB = 4 * S;
+    static constexpr int ND = rsa_f64_digits(S);      // 40 at S = 64, 20 at S = 32
+    static constexpr int TILES = (S == 64) ? 2 : RSA_TC_TILES32;
+    static constexpr int BLOCK = TILES * tc::TILE;
+    static constexpr int TMEM_COLS = (KB * TILES <= 256) ? 256 : 512;
+    static_assert(KB * TILES <= 512, "TMEM: KB columns per tile");
+};
 
-__global__ void __launch_bounds__(TC_BLOCK, 1) modexp_tc_kernel(const __grid_constant__ ModexpTcParams<TC_S> p) {
-    constexpr int ND = TC_ND, NP = ND / 2, NW = tc::NW;
+template <int S>
+__global__ void __launch_bounds__(TcCfg<S>::BLOCK, 1) modexp_tc_kernel(const __grid_constant__ ModexpTcParams<S> p) {
+    using C = TcCfg<S>;
+    constexpr int TC_S = S, TC_BLOCK = C::BLOCK;
+    constexpr int ND = C::ND, NP = ND / 2, NW = tc::Geom<C::KB>::NW;
+    using Shared = tc::TcShared<C::KB, C::TILES>;
     extern __shared__ __align__(1024) uint8_t smem_raw[];
-    tc::TcShared& sh = *reinterpret_cast<tc::TcShared*>(smem_raw);
-    double* const bslot = reinterpret_cast<double*>(smem_raw + sizeof(tc::TcShared)) + threadIdx.x;
+    Shared& sh = *reinterpret_cast<Shared*>(smem_raw);
+    double* const bslot = reinterpret_cast<double*>(smem_raw + sizeof(Shared)) + threadIdx.x;
     __shared__ __align__(16) double r2d[ND];
     const ModexpParams<TC_S>& ip = p.f.ip;
     const int warp = threadIdx.x / 32;
-    if (warp == 0) tc::tmem_alloc(tc::smem_u32(&sh.tmem_base), 512);
+    if (warp == 0) tc::tmem_alloc(tc::smem_u32(&sh.tmem_base), C::TMEM_COLS);
     if (threadIdx.x == 0) {
-        tc::mbar_init(tc::smem_u32(&sh.mbar[0]), 1);
-        tc::mbar_init(tc::smem_u32(&sh.mbar[1]), 1);
+        for (int i = 0; i < C::TILES; i++) tc::mbar_init(tc::smem_u32(&sh.mbar[i]), 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     tc::build_strips(sh, p.npb, reinterpret_cast<const uint8_t*>(ip.n));
@@ -70,7 +89,7 @@ __global__ void __launch_bounds__(TC_BLOCK, 1) modexp_tc_kernel(const __grid_con
     tc::TcTile tt;
     tt.tile = threadIdx.x / tc::TILE;
     tt.r = threadIdx.x % tc::TILE;
-    tt.tmem = sh.tmem_base + 256 * tt.tile;
+    tt.tmem = sh.tmem_base + C::KB * tt.tile;
     tt.tlane = (uint32_t)(32 * (warp % 4)) << 16;
     tt.mbar = tc::smem_u32(&sh.mbar[tt.tile]);
     tt.phase = 0;
@@ -152,7 +171,11 @@ __global__ void __launch_bounds__(TC_BLOCK, 1) modexp_tc_kernel(const __grid_con
                 tcd::Packer<2 * NW, decltype(word)> pk{word, 0};
                 auto put = [&](int k, uint64_t d) { pk.put(k, d); };
                 if (op.kind == RSA_OP_SQR) {
-                    f64::sqr_scan<ND>(a, put);
+                    if constexpr ((S == 32 && RSA_TC_SQREC32) || (S == 64 && RSA_TC_SQREC64))
+                        f64::sqr_col<ND, 0>(a, 0, 0, 0, put);   // compile-time-expanded scan (the loop form
+                                                                // is not unrolled at ND = 20 here)
+                    else
+                        f64::sqr_scan<ND>(a, put);
                 } else {
                     // rows, rolled (the unrolled column scan is ~160 KB of code);
                     // T's low digits go back into b's slot as b's digits are used up
@@ -187,31 +210,37 @@ __global__ void __launch_bounds__(TC_BLOCK, 1) modexp_tc_kernel(const __grid_con
     __syncthreads();
     if (warp == 0) {
         tc::fence_after();
-        tc::tmem_dealloc(sh.tmem_base, 512);
+        tc::tmem_dealloc(sh.tmem_base, C::TMEM_COLS);
     }
 }
 
-static size_t tc_smem_bytes() { return sizeof(tc::TcShared) + sizeof(double) * TC_ND * TC_BLOCK; }
+template <int S>
+static size_t tc_smem_bytes() {
+    return sizeof(tc::TcShared<TcCfg<S>::KB, TcCfg<S>::TILES>) + sizeof(double) * TcCfg<S>::ND * TcCfg<S>::BLOCK;
+}
 
+template <int S>
 static cudaError_t launch_tc(const void* params, int sms, cudaStream_t stream, int* grid_out, int* block_out,
                              size_t* slots_out, bool query_only) {
-    const int block = TC_BLOCK;
-    const size_t smem = tc_smem_bytes();
+    const int block = TcCfg<S>::BLOCK;
+    const size_t smem = tc_smem_bytes<S>();
     static OccCache cache;
     int occ = 0;
     cudaError_t ce = cached_occupancy(
-        cache, [&](int* o) { return occupancy_with_smem(modexp_tc_kernel, block, smem, o); }, &occ);
+        cache, [&](int* o) { return occupancy_with_smem(modexp_tc_kernel<S>, block, smem, o); }, &occ);
     if (ce != cudaSuccess) return ce;
-    if (occ > 1) occ = 1;   // one CTA per SM: each CTA allocates all 512 TMEM columns
+    // resident CTAs per SM: TMEM holds 512 columns
+    const int tmem_cap = 512 / TcCfg<S>::TMEM_COLS;
+    if (occ > tmem_cap) occ = tmem_cap;
     int grid = sms * occ;
     if (grid_out) *grid_out = grid;
     if (block_out) *block_out = block;
     if (slots_out) *slots_out = (size_t)grid * block;
     if (query_only) return cudaSuccess;
-    const ModexpTcParams<TC_S>& prm = *static_cast<const ModexpTcParams<TC_S>*>(params);
+    const ModexpTcParams<S>& prm = *static_cast<const ModexpTcParams<S>*>(params);
     const unsigned long long need = (prm.f.ip.count + block - 1) / block;
     if (need < (unsigned long long)grid) grid = (int)need;
-    modexp_tc_kernel<<<grid, block, smem, stream>>>(prm);
+    modexp_tc_kernel<S><<<grid, block, smem, stream>>>(prm);
     return cudaGetLastError();
 }
 
@@ -219,6 +248,9 @@ static cudaError_t launch_tc(const void* params, int sms, cudaStream_t stream, i
 
 cudaError_t rsa_b200_launch_tc(int S, const void* params, int sms, cudaStream_t stream, int* grid, int* block,
                                size_t* slots, bool query_only) {
-    if (S != rsa_b200::TC_S) return cudaErrorInvalidValue;
-    return rsa_b200::launch_tc(params, sms, stream, grid, block, slots, query_only);
+    switch (S) {
+    case 32: return rsa_b200::launch_tc<32>(params, sms, stream, grid, block, slots, query_only);
+    case 64: return rsa_b200::launch_tc<64>(params, sms, stream, grid, block, slots, query_only);
+    default: return cudaErrorInvalidValue;
+    }
 }

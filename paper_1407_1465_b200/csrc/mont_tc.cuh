@@ -1,5 +1,7 @@
 // mont_tc.cuh -- Montgomery reduction of a 128-packet tile on the tensor core
-// (2048-bit class: R = 2^2048, n < R odd, byte digits for the MMAs).
+// (operands of KB bytes, R = 2^(8 KB), n < R odd, byte digits for the MMAs;
+// KB = 256 for the 2048-bit class, 128 for the 1024-bit class.  The numbers
+// below are for KB = 256; every column index scales with KB).
 //
 // The operation is the reduction half of Fig 3's "(u*v) mod m" (PAPER.md:89,
 // sec. 3.6.1) realised by Montgomery's method, in
@@ -35,70 +37,88 @@
 namespace rsa_b200 {
 namespace tc {
 
-constexpr int KB = 256;                       // bytes per operand (R = 2^2048)
-constexpr int NW = 64;                        // 32-bit words per operand
 constexpr int TILE = 128;                     // packets per tile (MMA M, TMEM lanes)
 constexpr int STAGE_LBO = TILE * 16;          // bytes between 16-byte K chunks of a staging buffer
-constexpr int STAGE_BYTES = KB / 16 * STAGE_LBO;   // 32 KB
-// n' strip: GEMM1 blocks c0 in {0, 128}, K blocks I <= (c0 + 127) / 32: rows
-// rho = c0 + nn - 32 I in [-96, 255]
-constexpr int NP_RHO0 = -96, NP_ROWS = 352, NP_LBO = NP_ROWS * 16;
-// n strip: GEMM2 c0 = 252, I = 0..7: rows [28, 507]
-constexpr int G2_C0 = 252;
-constexpr int N_RHO0 = G2_C0 - 224, N_ROWS = 480, N_LBO = N_ROWS * 16;
-constexpr int NP_STRIP_BYTES = 2 * NP_LBO, N_STRIP_BYTES = 2 * N_LBO;
 
+// Geometry for operands of KB bytes (R = 2^(8 KB); KB = 256 at 2048 bits, 128 at 1024)
+template <int KB_>
+struct Geom {
+    static constexpr int KB = KB_;
+    static constexpr int NW = KB / 4;                         // 32-bit words per operand
+    static constexpr int STAGE_BYTES = KB / 16 * STAGE_LBO;   // 128 rows x KB bytes
+    // n' strip: GEMM1 blocks c0 = 128 b, K blocks I <= 4 b + 3: rows rho = c0 + nn - 32 I in [-96, KB)
+    static constexpr int NP_RHO0 = -96, NP_ROWS = KB + 96, NP_LBO = NP_ROWS * 16;
+    // n strip: GEMM2 columns G2_C0 .. G2_C0 + KB - 1, K blocks 0 .. KB/32 - 1: rows [28, 2 KB - 5]
+    static constexpr int G2_C0 = KB - 4;
+    static constexpr int N_RHO0 = G2_C0 - (KB - 32), N_ROWS = 2 * KB - 32, N_LBO = N_ROWS * 16;
+    static constexpr int NP_STRIP_BYTES = 2 * NP_LBO, N_STRIP_BYTES = 2 * N_LBO;
+    static constexpr int G2_N = KB < 256 ? KB : 256;          // MMA N of GEMM2 (one N block per K block)
+    static_assert(KB == 128 || KB == 256, "one GEMM2 N block");
+};
+
+template <int KB, int TILES>
 struct __align__(16) TcShared {
-    uint8_t stage[2][STAGE_BYTES];            // per tile: T_low, then m
-    uint8_t np_strip[NP_STRIP_BYTES];
-    uint8_t n_strip[N_STRIP_BYTES];
-    uint32_t nw[NW];                          // n as words (conditional subtraction)
-    unsigned long long mbar[2];
+    using G = Geom<KB>;
+    uint8_t stage[TILES][G::STAGE_BYTES];     // per tile: T_low, then m
+    uint8_t np_strip[G::NP_STRIP_BYTES];
+    uint8_t n_strip[G::N_STRIP_BYTES];
+    uint32_t nw[G::NW];                       // n as words (conditional subtraction)
+    unsigned long long mbar[TILES];
     uint32_t tmem_base;
 };
 
-// strip byte (chunk q, row rho, byte b) = y_{rho - 16 q - b} (0 outside [0, 256))
-__device__ __forceinline__ void build_strips(TcShared& sh, const uint8_t* __restrict__ npb,
+// strip byte (chunk q, row rho, byte b) = y_{rho - 16 q - b} (0 outside [0, KB))
+template <int KB, int TILES>
+__device__ __forceinline__ void build_strips(TcShared<KB, TILES>& sh, const uint8_t* __restrict__ npb,
                                              const uint8_t* __restrict__ nb) {
-    for (int i = threadIdx.x; i < NP_STRIP_BYTES; i += blockDim.x) {
-        const int q = i / NP_LBO, rem = i % NP_LBO, rho = rem / 16 + NP_RHO0, b = rem % 16;
+    using G = Geom<KB>;
+    for (int i = threadIdx.x; i < G::NP_STRIP_BYTES; i += blockDim.x) {
+        const int q = i / G::NP_LBO, rem = i % G::NP_LBO, rho = rem / 16 + G::NP_RHO0, b = rem % 16;
         const int idx = rho - 16 * q - b;
         sh.np_strip[i] = (idx >= 0 && idx < KB) ? npb[idx] : 0;
     }
-    for (int i = threadIdx.x; i < N_STRIP_BYTES; i += blockDim.x) {
-        const int q = i / N_LBO, rem = i % N_LBO, rho = rem / 16 + N_RHO0, b = rem % 16;
+    for (int i = threadIdx.x; i < G::N_STRIP_BYTES; i += blockDim.x) {
+        const int q = i / G::N_LBO, rem = i % G::N_LBO, rho = rem / 16 + G::N_RHO0, b = rem % 16;
         const int idx = rho - 16 * q - b;
         sh.n_strip[i] = (idx >= 0 && idx < KB) ? nb[idx] : 0;
     }
 }
 
 // staging address of 16-byte chunk c (bytes 16c .. 16c+15) of tile row r
-__device__ __forceinline__ uint4* stage_chunk(TcShared& sh, int tile, int r, int c) {
+template <int KB, int TILES>
+__device__ __forceinline__ uint4* stage_chunk(TcShared<KB, TILES>& sh, int tile, int r, int c) {
     return reinterpret_cast<uint4*>(sh.stage[tile] + c * STAGE_LBO + r * 16);
 }
 
-__device__ __forceinline__ void issue_gemm1(TcShared& sh, int tile, uint32_t tmem) {
+// GEMM1 (m's columns 0 .. KB-1): N = 128 blocks c0 = 128 b with K blocks
+// 0 .. 4b+3 (the rest of the block-triangle is zero)
+template <int KB, int TILES>
+__device__ __forceinline__ void issue_gemm1(TcShared<KB, TILES>& sh, int tile, uint32_t tmem) {
+    using G = Geom<KB>;
     const uint32_t st = smem_u32(sh.stage[tile]), sp = smem_u32(sh.np_strip);
     constexpr uint32_t id = idesc_u8(128, 128);
 #pragma unroll
-    for (int blk = 0; blk < 2; blk++) {
+    for (int blk = 0; blk < KB / 128; blk++) {
         const int c0 = 128 * blk;
 #pragma unroll
         for (int I = 0; I < 4 + 4 * blk; I++) {
             const uint64_t a = sdesc(st + 2 * I * STAGE_LBO, STAGE_LBO, 128);
-            const uint64_t b = sdesc(sp + (c0 - 32 * I - NP_RHO0) * 16, NP_LBO, 128);
+            const uint64_t b = sdesc(sp + (c0 - 32 * I - G::NP_RHO0) * 16, G::NP_LBO, 128);
             mma_u8(tmem + c0, a, b, id, I > 0);
         }
     }
 }
 
-__device__ __forceinline__ void issue_gemm2(TcShared& sh, int tile, uint32_t tmem) {
+// GEMM2 (columns G2_C0 .. G2_C0 + KB - 1 of m n): one N = KB block per K block
+template <int KB, int TILES>
+__device__ __forceinline__ void issue_gemm2(TcShared<KB, TILES>& sh, int tile, uint32_t tmem) {
+    using G = Geom<KB>;
     const uint32_t st = smem_u32(sh.stage[tile]), sn = smem_u32(sh.n_strip);
-    constexpr uint32_t id = idesc_u8(128, 256);
+    constexpr uint32_t id = idesc_u8(128, G::G2_N);
 #pragma unroll
-    for (int I = 0; I < 8; I++) {
+    for (int I = 0; I < KB / 32; I++) {
         const uint64_t a = sdesc(st + 2 * I * STAGE_LBO, STAGE_LBO, 128);
-        const uint64_t b = sdesc(sn + (G2_C0 - 32 * I - N_RHO0) * 16, N_LBO, 128);
+        const uint64_t b = sdesc(sn + (G::G2_C0 - 32 * I - G::N_RHO0) * 16, G::N_LBO, 128);
         mma_u8(tmem, a, b, id, I > 0);
     }
 }
@@ -154,7 +174,10 @@ struct TcTile {
 // Carries: word w of a GEMM's output is P_w = sum_i c_{4w+i} 2^(8i) < 2^50,
 // computed for 8 words at a time independently; the words then follow from
 // one add-with-carry chain lo(P_w) + hi(P_{w-1}) + carry.
-__device__ __forceinline__ void redc(TcShared& sh, TcTile& tt, uint32_t t63, uint32_t (&th)[NW]) {
+template <int KB, int TILES>
+__device__ __forceinline__ void redc(TcShared<KB, TILES>& sh, TcTile& tt, uint32_t t63,
+                                     uint32_t (&th)[Geom<KB>::NW]) {
+    constexpr int NW = Geom<KB>::NW, NCH = KB / 32;   // words, 32-column TMEM chunks
     const int tile = tt.tile, r = tt.r;
     // ---- GEMM1: m's column sums
     fence_async_smem();
@@ -171,7 +194,7 @@ __device__ __forceinline__ void redc(TcShared& sh, TcTile& tt, uint32_t t63, uin
     uint32_t hprev = 0;
     uint32_t m253 = 0, m254 = 0, m255 = 0;
 #pragma unroll
-    for (int ch = 0; ch < 8; ch++) {
+    for (int ch = 0; ch < NCH; ch++) {
         uint32_t v[32];
         tmem_ld32(tt.tmem + tt.tlane + 32 * ch, v);
         tmem_ld_wait();
@@ -188,7 +211,7 @@ __device__ __forceinline__ void redc(TcShared& sh, TcTile& tt, uint32_t t63, uin
         hprev = addc(hi[7], 0u);
         *stage_chunk(sh, tile, r, 2 * ch) = make_uint4(w[0], w[1], w[2], w[3]);
         *stage_chunk(sh, tile, r, 2 * ch + 1) = make_uint4(w[4], w[5], w[6], w[7]);
-        if (ch == 7) {
+        if (ch == NCH - 1) {               // m's top bytes KB-3 .. KB-1
             m253 = (w[7] >> 8) & 0xFF;
             m254 = (w[7] >> 16) & 0xFF;
             m255 = w[7] >> 24;
@@ -203,7 +226,7 @@ __device__ __forceinline__ void redc(TcShared& sh, TcTile& tt, uint32_t t63, uin
         issue_gemm2(sh, tile, tt.tmem);
         commit(tt.mbar);
     }
-    // columns 508..510 (the top byte products) meanwhile
+    // columns 2KB-4 .. 2KB-2 (the top byte products) meanwhile
     const uint32_t n63 = sh.nw[NW - 1];
     const uint32_t n253 = n63 >> 8 & 0xFF, n254 = n63 >> 16 & 0xFF, n255 = n63 >> 24;
     const uint32_t c508 = m253 * n255 + m254 * n254 + m255 * n253;
@@ -212,12 +235,12 @@ __device__ __forceinline__ void redc(TcShared& sh, TcTile& tt, uint32_t t63, uin
     mbar_wait(tt.mbar, tt.phase);
     tt.phase ^= 1;
     fence_after();
-    // TMEM column idx = global column 252 + idx.  Word w of U (bits 2048 + 32 w)
-    // is P_w over global columns 256 + 4w .. 259 + 4w = idx 4 + 4w .. 7 + 4w.
+    // TMEM column idx = global column KB-4 + idx.  Word w of U (bits 8 KB + 32 w)
+    // is P_w over global columns KB + 4w .. KB + 3 + 4w = idx 4 + 4w .. 7 + 4w.
     // The carry V out of the low half enters as the "previous high" of word 0.
     uint32_t carry = 0;
 #pragma unroll
-    for (int ch = 0; ch < 8; ch++) {
+    for (int ch = 0; ch < NCH; ch++) {
         uint32_t v[32];
         tmem_ld32(tt.tmem + tt.tlane + 32 * ch, v);
         tmem_ld_wait();
@@ -248,7 +271,7 @@ __device__ __forceinline__ void redc(TcShared& sh, TcTile& tt, uint32_t t63, uin
         for (int q = q0 + 1; q < 8; q++) th[w0 + q] = addc_cc(th[w0 + q], x[q]);
         carry = addc(0u, 0u);
     }
-    // word 63 = columns 508..511 (idx 256..259, past the last chunk), then bit 2048
+    // word NW-1 = columns 2KB-4 .. 2KB-1 (past the last chunk), then bit 8 KB
     {
         const uint64_t p = col4(c508, c509, c510, 0) + hprev + carry;
         th[NW - 1] = add_cc(th[NW - 1], (uint32_t)p);

@@ -217,12 +217,12 @@ static void fill_tc(ModexpTcParams<S>* t, const BN& n) {
 
 template <int S>
 static void fill_params(Plan& pl, const BN& n, const std::vector<RsaOp>& ops) {
-    if constexpr (S == 64) {
+    if constexpr (S == 64 || S == 32) {
         // FP64 params + the tensor-core kernel's n' (one blob serves every path of the class)
         pl.params.assign(sizeof(ModexpTcParams<S>), 0);
         fill_f64<S>(reinterpret_cast<ModexpF64Params<S>*>(pl.params.data()), n);
         if (pl.path == RSA_PATH_TC) fill_tc<S>(reinterpret_cast<ModexpTcParams<S>*>(pl.params.data()), n);
-    } else if constexpr (S == 32 || S == 128) {
+    } else if constexpr (S == 128) {
         pl.params.assign(sizeof(ModexpF64Params<S>), 0);
         fill_f64<S>(reinterpret_cast<ModexpF64Params<S>*>(pl.params.data()), n);
     } else {
