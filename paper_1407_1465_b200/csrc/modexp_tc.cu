@@ -40,7 +40,16 @@ namespace rsa_b200 {
 #define RSA_TC_SQREC32 1
 #endif
 #ifndef RSA_TC_SQREC64
-#define RSA_TC_SQREC64 0
+#define RSA_TC_SQREC64 1
+#endif
+#ifndef RSA_TC_SQB64
+#define RSA_TC_SQB64 2      // products per batch of the scan, A/B at 2048 bits: 2/4/6/8 -> 949-953K/942K/955K/947K
+#endif
+#ifndef RSA_TC_SQB32
+#define RSA_TC_SQB32 4      // ... CRT-2048 (1024-bit halves): 2/4/6 -> 3.20M/3.24M/3.24M
+#endif
+#ifndef RSA_TC_SQACC2
+#define RSA_TC_SQACC2 0     // two partial sums per column (A/B: 927K vs 953K at 2048 bits)
 #endif
 #ifndef RSA_TC_LOCK
 #define RSA_TC_LOCK 1   // both tiles start every op together (A/B: 900.5K vs 809K: the unrolled squaring is
@@ -172,8 +181,9 @@ __global__ void __launch_bounds__(TcCfg<S>::BLOCK, 1) modexp_tc_kernel(const __g
                 auto put = [&](int k, uint64_t d) { pk.put(k, d); };
                 if (op.kind == RSA_OP_SQR) {
                     if constexpr ((S == 32 && RSA_TC_SQREC32) || (S == 64 && RSA_TC_SQREC64))
-                        f64::sqr_col<ND, 0>(a, 0, 0, 0, put);   // compile-time-expanded scan (the loop form
-                                                                // is not unrolled at ND = 20 here)
+                        // the compile-time-expanded scan (the loop form is not unrolled at ND = 20
+                        // here; at ND = 40, A/B: 949K vs 901K decrypts/s)
+                        f64::sqr_col<ND, 0, (S == 64 ? RSA_TC_SQB64 : RSA_TC_SQB32), RSA_TC_SQACC2>(a, 0, 0, 0, put);
                     else
                         f64::sqr_scan<ND>(a, put);
                 } else {

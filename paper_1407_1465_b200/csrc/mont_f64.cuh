@@ -371,7 +371,7 @@ __host__ __device__ constexpr int sqr_ncross(int k) {
 // until then (at ND = 80 the ~40 pending highs would take 80 registers next to
 // A's 160 and starve the product schedule); lows and highs are added two
 // products at a time (3-input 64-bit adds).
-template <int ND, int K, typename Put>
+template <int ND, int K, int SQB_ = RSA_F64_SQBATCH, int ACC2 = RSA_F64_SQACC2, typename Put>
 __host__ __device__ __forceinline__ void sqr_col(const double (&a)[ND], uint64_t xh, uint64_t hd, uint64_t carry,
                                                  Put& put) {
     if constexpr (K < 2 * ND) {
@@ -380,7 +380,7 @@ __host__ __device__ __forceinline__ void sqr_col(const double (&a)[ND], uint64_t
         uint64_t x = xh, xn = 0, x2 = 0, xn2 = 0;
         // products in batches of SQB (every h, then every s = C2 - h, then every
         // l): the batch is the number of exact splits in flight per warp
-        constexpr int SQB = RSA_F64_SQBATCH;
+        constexpr int SQB = SQB_;
 #pragma unroll
         for (int m0 = 0; m0 < NH; m0 += SQB) {
             double hb[SQB], lb[SQB];
@@ -396,8 +396,8 @@ __host__ __device__ __forceinline__ void sqr_col(const double (&a)[ND], uint64_t
 #pragma unroll
             for (int u = 0; u < SQB; u += 2) {
                 // RSA_F64_SQACC2: alternate pairs go to second partial sums
-                uint64_t& xs = (RSA_F64_SQACC2 && ((m0 + u) / 2) % 2) ? x2 : x;
-                uint64_t& xns = (RSA_F64_SQACC2 && ((m0 + u) / 2) % 2) ? xn2 : xn;
+                uint64_t& xs = (ACC2 && ((m0 + u) / 2) % 2) ? x2 : x;
+                uint64_t& xns = (ACC2 && ((m0 + u) / 2) % 2) ? xn2 : xn;
                 if (m0 + u + 1 < NH) {
                     xs += bits(lb[u]) + bits(lb[u + 1]);
                     xns += bits(hb[u]) + bits(hb[u + 1]);
@@ -424,7 +424,7 @@ __host__ __device__ __forceinline__ void sqr_col(const double (&a)[ND], uint64_t
         }
         const uint64_t v = 2 * (x - XB) + (y - yb) + carry;
         put(K, v & M52);
-        sqr_col<ND, K + 1>(a, xn, hdn, v >> D, put);
+        sqr_col<ND, K + 1, SQB_, ACC2>(a, xn, hdn, v >> D, put);
     }
 }
 
