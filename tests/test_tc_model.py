@@ -57,10 +57,18 @@ def test_product_words(model, op):
         assert model(f"{op} {a:x} {b:x}") == a * b
 
 
-def test_square_words(model):
+@pytest.mark.parametrize("op", ["Q", "R"])
+def test_square_words(model, op):
     rng = random.Random(9)
     for a, _ in operands(rng):
-        assert model(f"Q {a:x}") == a * a
+        assert model(f"{op} {a:x}") == a * a
+
+
+def test_square_words_1024(model):
+    rng = random.Random(11)
+    for a, _ in operands(rng):
+        a &= (1 << 1024) - 1
+        assert model(f"H {a:x}") == a * a
 
 
 def test_words_digits_roundtrip(model):
