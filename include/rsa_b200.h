@@ -216,10 +216,14 @@ typedef struct {
     long long products;   /* algorithmic 32x32->64 limb products per packet: squarings x
                              (1.5S^2+1.5S or 2S^2+S) + other montmuls x (2S^2+S) */
     int fp64_digits;      /* 0: the class runs on the integer (IMAD) pipe; else ND, the
-                             number of 52-bit digits of the FP64-pipe kernel (mont_f64.cuh) */
-    long long digit_products; /* FP64-pipe kernel: 52x52-bit digit products per packet, each
-                             2 DFMA + 1 DADD: squarings x (ND(ND+1)/2 + ND^2) + other
-                             montmuls x 2 ND^2; 0 for integer-pipe classes */
+                             number of 52-bit digits of the FP64-pipe arithmetic (mont_f64.cuh;
+                             also the product half of the tensor-core path) */
+    long long digit_products; /* 52x52-bit digit products per packet on the FP64 pipe, each
+                             2 DFMA + 1 DADD.  FP64 kernel: squarings x (ND(ND+1)/2 + ND^2) +
+                             other montmuls x 2 ND^2.  Tensor-core path (RSA_PATH_TC): the
+                             product T = A B only, squarings x ND(ND+1)/2 + other montmuls x
+                             ND^2 (the reduction runs on the tensor core).  0 for
+                             integer-pipe classes */
 } rsa_plan_info_t;
 
 int rsa_plan_info(const uint32_t* exp, const uint32_t* n, int nbits, rsa_plan_info_t* info);

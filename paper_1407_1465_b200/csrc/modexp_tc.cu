@@ -142,7 +142,9 @@ __global__ void __launch_bounds__(TcCfg<S>::BLOCK, 1) modexp_tc_kernel(const __g
                     a[2 * g + 1] = v.y;
                 }
             }
-            // the second operand of a multiply goes to this thread's slot
+            // the second operand of a multiply goes to this thread's slot (once per op: only
+            // squarings repeat, rep > 1; the plan builder guarantees rep == 1 for the others,
+            // whose row-form product overwrites the slot with T's low digits)
             if (op.kind == RSA_OP_MUL) {
 #pragma unroll
                 for (int g = 0; g < NP; g++) {

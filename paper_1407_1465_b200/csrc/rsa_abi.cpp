@@ -236,7 +236,11 @@ static void fill_params(Plan& pl, const BN& n, const std::vector<RsaOp>& ops) {
     rsa_host::to_limbs(n, p->n, S);
     BN r2 = rsa_host::pow2_mod(64 * S, n);      // R^2 mod n, R = 2^(32 S)
     rsa_host::to_limbs(r2, p->r2, S);
-    for (size_t i = 0; i < ops.size(); i++) p->ops[i] = ops[i];
+    for (size_t i = 0; i < ops.size(); i++) {
+        // only squarings repeat (the kernels stage a multiply's operand once per op)
+        if (ops[i].kind != RSA_OP_SQR && ops[i].rep != 1) abort();
+        p->ops[i] = ops[i];
+    }
 }
 
 template <int S>

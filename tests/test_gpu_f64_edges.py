@@ -1,5 +1,7 @@
-"""Structured edge moduli for the FP64-pipe kernels (paper_1407_1465_b200/csrc/
-mont_f64.cuh; the default for the 1024-, 2048- and 4096-bit classes): moduli
+"""Structured edge moduli for the FP64-pipe arithmetic (paper_1407_1465_b200/csrc/
+mont_f64.cuh: the whole multiply at 4096 bits; the product half of the
+tensor-core kernels, the default at 513-2048 bits, whose n' = -n^-1 mod R
+then takes its extreme byte patterns too): moduli
 whose 52-bit digits are all ones or nearly all zeros (every column at its
 carry extreme), the smallest and largest modulus of each class (R / n from
 2^4 to 2^1056), bases at 0, 1, n - 1, n, 2^(32 s) - 1 (the call is total), and
@@ -37,8 +39,19 @@ def moduli(nb):
     ]
 
 
-@pytest.mark.parametrize("nb", [513, 1000, 1024, 1025, 1536, 2047, 2048, 2049, 3072, 4095, 4096])
-def test_f64_edge_moduli(R, nb):
+@pytest.mark.parametrize("nb,path", [(513, None), (1000, None), (1024, None), (1025, None), (1536, None),
+                                     (2047, None), (2048, None), (2049, None), (3072, None), (4095, None),
+                                     (4096, None), (1024, "FP64"), (2048, "FP64"), (1025, "FP64")])
+def test_f64_edge_moduli(R, nb, path):
+    if path is None:
+        _edges(R, nb)
+    else:                                   # the FP64 kernel, selectable where the TC path is the default
+        with R.kernel_path(next(c for c in (32, 64, 128) if workload.limbs_needed(nb) <= c),
+                           getattr(R, "RSA_PATH_" + path)):
+            _edges(R, nb)
+
+
+def _edges(R, nb):
     rnd = random.Random(52 * nb)
     s = workload.limbs_needed(nb)
     full = (1 << (32 * s)) - 1
