@@ -52,10 +52,12 @@ def build(force: bool = False, verbose: bool = False, out: str | None = None) ->
     _compile_link(LIB + ".tmp", extra, verbose)
     os.replace(LIB + ".tmp", LIB)
     # the microbenchmarks (roofline denominator, chain latency), built alongside
-    for name in ("imad_peak", "imad_latency", "dfma_latency"):
+    for name in ("imad_peak", "imad_latency", "dfma_latency", "tc_redc"):
         mb = os.path.join(CSRC, "microbench", name)
         src = mb + ".cu"
-        if os.path.exists(src) and (force or not os.path.exists(mb) or os.path.getmtime(mb) < os.path.getmtime(src)):
+        # tc_redc includes the product headers (mont_tc.cuh): rebuilt with the library
+        if os.path.exists(src) and (force or name == "tc_redc" or not os.path.exists(mb)
+                                    or os.path.getmtime(mb) < os.path.getmtime(src)):
             subprocess.check_call([NVCC, *ARCH, "-O3", "-lineinfo", "-o", mb, src])
     return LIB
 
