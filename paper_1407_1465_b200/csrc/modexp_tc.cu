@@ -1,28 +1,32 @@
 // modexp_tc.cu -- batched modular exponentiation with the Montgomery
-// reduction on the tensor core (sm_100a), width class S = 64 (1025..2048-bit
-// moduli).
+// reduction on the tensor core (sm_100a), width classes S = 64 (1025..2048-bit
+// moduli) and S = 32 (513..1024 bits; also the CRT halves of RSA-2048).
 //
 // Same contract and op list as modexp_kernel / modexp_f64_kernel: out[i] =
 // base[i]^exp mod n for every packet (sec. 2, sec.
 // 3.3), one thread per packet, the shared exponent's op list executed
-// warp-uniformly.  Each Montgomery multiply A <- A B R^-1 mod n (R = 2^2048)
+// warp-uniformly.  Each Montgomery multiply A <- A B R^-1 mod n (R = 2^(32 S))
 // is split between the two engines of the SM:
 //   CUDA cores (FP64 pipe): T = A B by product scanning (tc_digits.cuh;
-//     squarings by f64::sqr_scan, ND (ND+1)/2 = 820 digit products instead of
-//     the 2420 of a full FP64 Montgomery squaring), streamed out as words:
-//     T_low into the tile's staging buffer, T_high into registers;
+//     squarings by the compile-time-expanded f64::sqr_col, ND (ND+1)/2 = 820
+//     digit products at S = 64 instead of the 2420 of a full FP64 Montgomery
+//     squaring; multiplies by the rolled row form tcd::mul_rows), streamed out
+//     as words: T_low into the tile's staging buffer, T_high into registers;
 //   tensor core: m = T_low n' mod R and the columns of m n (mont_tc.cuh),
 //     the carries resolved by each packet's thread; U < n after one
 //     conditional subtraction (so every intermediate is canonical).
-// CTA = two tiles of 128 packets (warps 0-3, 4-7), one CTA per SM (255
-// registers): while one tile waits for its MMAs the other one's warps run.
-// Each tile owns 256 TMEM columns and a mbarrier; the tiles synchronise
-// only with named barriers of their own 128 threads.
+// CTA = TILES tiles of 128 packets (2 at S = 64: 255 registers; 4 at S = 32:
+// 128 registers), one CTA per SM; each tile owns KB TMEM columns and an
+// mbarrier and synchronises its MMAs with named barriers of its own 128
+// threads; all tiles start every Montgomery op together (RSA_TC_LOCK: the
+// unrolled squaring is ~85 KB of SASS, and tiles on different code lines
+// stall on instruction fetch).
 //
-// Shared memory: TcShared (n' and n Toeplitz strips, 2 x 32 KB staging) and a
-// per-thread B slot (ND doubles, digit-major across the block) for the
-// multiplies' second operand.  The window table is the FP64 kernel's format
-// (entries as digit pairs, entry-major then pair-major across the grid).
+// Shared memory: TcShared (n' and n Toeplitz strips, TILES x 128 x KB-byte
+// staging) and a per-thread B slot (ND doubles, digit-major across the
+// block) for the multiplies' second operand.  The window table is the FP64
+// kernel's format (entries as digit pairs, entry-major then pair-major
+// across the grid).
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -37,10 +41,10 @@ namespace rsa_b200 {
 #define RSA_TC_TILES32 4    // 1024-bit class: tiles of 128 packets per CTA (TMEM 128 columns each)
 #endif
 #ifndef RSA_TC_SQREC32
-#define RSA_TC_SQREC32 1
-#endif
+#define RSA_TC_SQREC32 1    // squarings by the compile-time-expanded scan (sqr_col) instead of the loop
+#endif                      // form (sqr_scan): A/B CRT-2048 3.24M vs 0.45M (loop not unrolled at ND = 20)
 #ifndef RSA_TC_SQREC64
-#define RSA_TC_SQREC64 1
+#define RSA_TC_SQREC64 1    // ... at 2048 bits: 949K vs 901K decrypts/s
 #endif
 #ifndef RSA_TC_SQB64
 #define RSA_TC_SQB64 2      // products per batch of the scan, A/B at 2048 bits: 2/4/6/8 -> 949-953K/942K/955K/947K
