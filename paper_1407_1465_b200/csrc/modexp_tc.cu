@@ -55,6 +55,9 @@ namespace rsa_b200 {
 #ifndef RSA_TC_SQACC2
 #define RSA_TC_SQACC2 0     // two partial sums per column (A/B: 927K vs 953K at 2048 bits)
 #endif
+#ifndef RSA_TC_LOCK32
+#define RSA_TC_LOCK32 0     // 1024-bit class: no CTA barrier per op (A/B: CRT-2048 3.44M vs 3.24M; its code is small)
+#endif
 #ifndef RSA_TC_LOCK
 #define RSA_TC_LOCK 1   // both tiles start every op together (A/B: 900.5K vs 809K: the unrolled squaring is
                         // ~85 KB of SASS and two tiles on different code lines stall on instruction fetch)
@@ -169,7 +172,7 @@ __global__ void __launch_bounds__(TcCfg<S>::BLOCK, 1) modexp_tc_kernel(const __g
                 for (int k = 0; k < ND; k++) bslot[k * TC_BLOCK] = (k == 0) ? 1.0 : 0.0;
             }
             for (int r = 0; r < op.rep; r++) {
-                if constexpr (RSA_TC_LOCK != 0) __syncthreads();   // A/B: both tiles on the same code lines
+                if constexpr ((S == 64 ? RSA_TC_LOCK : RSA_TC_LOCK32) != 0) __syncthreads();   // all tiles on the same code lines
                 // T = A B: words 0..63 to the staging buffer (16-byte chunks), 64..127 to th
                 uint32_t t63 = 0, wb0 = 0, wb1 = 0, wb2 = 0;
                 auto word = [&](int w, uint32_t v) {
