@@ -266,6 +266,21 @@ def measured_digit_mix_rate():
     return best
 
 
+def measured_i8_tops():
+    """Best int8 tcgen05.mma rate (T int8-op/s, whole GPU) measured by
+    csrc/microbench/tc_i8_peak.cu (profiles/r02_tc_i8_peak.jsonl), or None."""
+    best = None
+    try:
+        with open(os.path.join(ROOT, "profiles", "r02_tc_i8_peak.jsonl")) as f:
+            for line in f:
+                if line.startswith("{"):
+                    v = json.loads(line).get("int8_tops")
+                    best = v if best is None or (v and v > best) else best
+    except (OSError, ValueError):
+        return None
+    return best
+
+
 def batch_kernel_name(R, S: int) -> str:
     """The kernel modexp.cu launches for width class S (its resolved path)."""
     path = R.rsa_get_kernel_path(S)
@@ -605,7 +620,8 @@ def run_ours(args, rank, world, local_rank):
         lane_ops = 5 * pd["digit_products"] + 4 * tc_words_per_op(S) * pd["montmuls"]
         l_ach = count * lane_ops / (leg_ms[dom] / 1e3) / 1e12
         l_peak = LANE_OPS_PER_CLK_PER_SM * sms * f_max * 1e6 / 1e12
-        i8_peak = 2 * float(peaks.get("bf16_tflops_sustained", 1378.2))      # int8 = 2 x bf16 (guide's ratio)
+        i8_meas = measured_i8_tops()
+        i8_peak = i8_meas or 2 * float(peaks.get("bf16_tflops_sustained", 1378.2))   # int8 = 2 x bf16
         i8_ach = count * 2 * tc_macs_per_op(S) * pd["montmuls"] / (leg_ms[dom] / 1e3) / 1e12
         roofline.update({
             "bound": "alu", "achieved": l_ach, "peak": l_peak, "unit": "T lane-op/s", "frac": l_ach / l_peak,
@@ -620,7 +636,10 @@ def run_ours(args, rank, world, local_rank):
             "tensor": {"achieved": i8_ach, "peak": i8_peak, "unit": "T int8-op/s", "frac": i8_ach / i8_peak,
                        "algorithmic": f"{tc_macs_per_op(S)} u8 MACs x 2 per packet per Montgomery op "
                                       f"(m = T n' mod R, columns of m n) x {pd['montmuls']} ops",
-                       "peak_source": "2 x MEASURED_PEAKS bf16_tflops_sustained (guide: int8/fp8 = 2 x bf16 dense)"},
+                       "peak_source": ("measured: best u8 tcgen05.mma rate of profiles/r02_tc_i8_peak.jsonl "
+                                       "(csrc/microbench/tc_i8_peak.cu, back-to-back M=128 N=256 K=32)")
+                                      if i8_meas else
+                                      "2 x MEASURED_PEAKS bf16_tflops_sustained (guide: int8/fp8 = 2 x bf16 dense)"},
             "imad_equiv": {"achieved": achieved, "peak": peak, "unit": "Tprod/s", "frac": achieved / peak,
                            "peak_source": "nominal (half-rate IMAD.WIDE, profiles/r01_imad_peak.jsonl)",
                            "basis": "the metric's '% of IMAD peak': the textbook 32x32->64 limb-product count "
