@@ -61,14 +61,23 @@ __device__ __forceinline__ void mbar_init(uint32_t mbar, uint32_t count) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(mbar), "r"(count) : "memory");
 }
 
+// Wait for the phase with the given parity to complete.  Bounded: a phase that
+// never completes (a malformed descriptor, a lost commit) traps after ~2^26
+// polls (seconds) instead of hanging the GPU; the launch then fails with an
+// error the host reports as RSA_ECUDA.
 __device__ __forceinline__ void mbar_wait(uint32_t mbar, uint32_t parity) {
-    asm volatile(
-        "{\n\t.reg .pred P1;\n"
-        "WAIT_%=:\n\t"
-        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
-        "@!P1 bra WAIT_%=;\n\t}\n" ::"r"(mbar),
-        "r"(parity)
-        : "memory");
+    uint32_t done = 0;
+    for (uint32_t tries = 0;; tries++) {
+        asm volatile(
+            "{\n\t.reg .pred P1;\n\t"
+            "mbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2;\n\t"
+            "selp.u32 %0, 1, 0, P1;\n\t}\n"
+            : "=r"(done)
+            : "r"(mbar), "r"(parity)
+            : "memory");
+        if (done) return;
+        if (tries > (1u << 26)) __trap();
+    }
 }
 
 // generic-proxy shared-memory writes -> visible to the tensor core (async proxy)
