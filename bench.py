@@ -412,7 +412,15 @@ def run_ours(args, rank, world, local_rank):
         mods = torch.from_numpy(np.ascontiguousarray(mods_np).view(np.int32)).to(dev)
         expt = torch.from_numpy(workload.ints_to_rows([ev] * 1, s).view(np.int32)).to(dev).expand(count, s).contiguous()
         exps = [ev]
-        plans = [R.rsa_multi_plan_info(nb, ev.bit_length())]
+        pm = R.rsa_multi_plan_info(nb, ev.bit_length())
+        # the kernel skips a window's multiply when every digit in the CTA is 0
+        # (modexp_multi.cu RSA_MULTI_SKIP0); this batch has one exponent, so the
+        # executed multiplies are the nonzero digits below the top window
+        w_, nwin_ = pm["window"], (ev.bit_length() + pm["window"] - 1) // pm["window"]
+        zero_ = sum(1 for wi in range(nwin_ - 1) if (ev >> (wi * w_)) & ((1 << w_) - 1) == 0)
+        S_ = pm["width_class"]
+        plans = [dict(pm, montmuls=pm["montmuls"] - zero_, products=pm["products"] - zero_ * (2 * S_ * S_ + S_),
+                      skipped_zero_windows=zero_)]
     elif kind == "crt":
         exps = [key["d"]]
         p_, q_ = max(key["p"], key["q"]), min(key["p"], key["q"])

@@ -6,7 +6,8 @@
 // One thread per packet.  Everything per-key is derived on the device:
 //   n'  = -n^-1 mod 2^32             (Newton, 5 steps)
 //   r1  = R mod n                    (2^b - n, then 32S - b modular doublings)
-//   R^2 mod n = Mont(2)^(2^k), k = log2(32 S)   (k Montgomery squarings)
+//   R^2 mod n = Mont(2^KD)^(2^J)     (KD more doublings, then J Montgomery
+//                                     squarings, KD 2^J = 32 S; plan.h)
 // The exponent is scanned with a FIXED window of w bits over a uniform bit
 // length (exp_bits), so every thread executes the same op sequence and only
 // the table index (its own digit) differs: no divergence despite per-packet
@@ -21,6 +22,7 @@
 
 #include "devcache.h"
 #include "mont_multi.cuh"
+#include "plan.h"
 
 namespace rsa_b200 {
 
@@ -45,6 +47,9 @@ template <int S>
 #endif
 #ifndef RSA_MMINB16
 #define RSA_MMINB16 4
+#endif
+#ifndef RSA_MULTI_SKIP0
+#define RSA_MULTI_SKIP0 1
 #endif
 #ifndef RSA_MULTI_NREG_MAX
 #define RSA_MULTI_NREG_MAX 32
@@ -151,8 +156,9 @@ modexp_multi_kernel(const __grid_constant__ MultiParams p) {
                 else if (b - lo < 32) a[k] &= (1u << (b - lo)) - 1u;
             }
         }
-        // v = 2v mod n, (32S - b) + 1 times: the last one gives Mont(2) = 2R mod n
-        for (int d = 0; d <= 32 * S - b; d++) {
+        // v = 2v mod n, (32S - b) + KD times: the last KD give Mont(2^KD) = 2^KD R mod n
+        constexpr int KD = MultiR2<S>::KD;
+        for (int d = 0; d < 32 * S - b + KD; d++) {
             if (d == 32 * S - b) store_a(0, a);          // T[0] = R mod n = Mont(1)
             uint32_t top = a[S - 1] >> 31;
             uint32_t sh[S];
@@ -186,12 +192,12 @@ modexp_multi_kernel(const __grid_constant__ MultiParams p) {
         }
         const int nwin = (ebits + w - 1) / w;
         // ---- step machine (one call site each for montsqr_sm / montmul_sm):
-        //  [0, K)                 SQR: Mont(2) -> R^2 mod n     (K = log2(32 S))
+        //  [0, K)                 SQR: Mont(2^KD) -> R^2 mod n  (K = J, plan.h)
         //  K                      MUL: x * R^2 -> T[1] = Mont(x)
         //  K+1 .. K+nent-2        MUL: T[j] = T[j-1] * T[1]
         //  scan                   per window below the top: w SQR + 1 MUL by T[digit]
         //  mode 0: 1 MUL by 1 (from Montgomery);  mode 1: r-1 SQR, compare with Mont(-1)
-        constexpr int K = (S == 8) ? 8 : (S == 16) ? 9 : (S == 32) ? 10 : 11;
+        constexpr int K = MultiR2<S>::SQ;
         const int s_tab = K + 1, s_scan = K + 1 + (nent - 2);
         const int s_fin = s_scan + (nwin - 1) * (w + 1);
         // lockstep (S >= 64): a barrier per step keeps the CTA's warps on the
@@ -242,6 +248,16 @@ modexp_multi_kernel(const __grid_constant__ MultiParams p) {
                 sqr = ph < w;
                 if (!sqr) {
                     const uint32_t dig = exp_bits_at(esrc, p.s_io, wi * w + eoff, w);
+                    // the multiply by T[0] = Mont(1) is the identity (mod n): a CTA (the
+                    // lockstep classes) or warp whose digits are all 0 skips it.  Sparse
+                    // exponents (e = 65537: 7 of 8 windows below the top at w = 2) gain
+                    // the most; the result is unchanged (RSA_MULTI_SKIP0 = 0 for A/B).
+                    if constexpr (RSA_MULTI_SKIP0 != 0) {
+                        bool any;
+                        if constexpr (S >= 64) any = __syncthreads_or(dig != 0u) != 0;
+                        else any = __any_sync(__activemask(), dig != 0u);
+                        if (!any) continue;
+                    }
 #pragma unroll
                     for (int g = 0; g < NG; g++) bslot[g * stride] = tab(dig, g);
                 }

@@ -91,6 +91,25 @@ struct ModexpTcParams {
     uint8_t npb[4 * S];                      // -n^-1 mod 2^(32 S), little-endian bytes
 };
 
+// Multi-key kernel (modexp_multi.cu) per-key R^2 mod n: Mont(2^KD) = 2^KD R mod
+// n by modular doublings of R mod n, then RSA_MULTI_R2SQ Montgomery squarings
+// ((2^KD R)^(2^J) R^-(2^J - 1) = 2^(KD 2^J) R = R^2 with KD 2^J = 32 S).  A
+// doubling is ~1/36 of a 2048-bit squaring, so J = 4 (KD = 128 at S = 64)
+// instead of J = log2(32 S) = 11 (KD = 1).
+#ifndef RSA_MULTI_R2SQ
+#define RSA_MULTI_R2SQ 4    // A/B multi-key RSA-2048 encrypt: J = 11 / 6 / 5 / 4 -> 23.2M / 26.1M / 26.6M / 26.8M
+#endif
+constexpr int rsa_log2_bits(int S) { return S <= 1 ? 5 : 1 + rsa_log2_bits(S / 2); }   // log2(32 S)
+constexpr int rsa_multi_r2_squarings(int S) {
+    return rsa_log2_bits(S) < RSA_MULTI_R2SQ ? rsa_log2_bits(S) : RSA_MULTI_R2SQ;
+}
+constexpr int rsa_multi_r2_doublings(int S) { return 1 << (rsa_log2_bits(S) - rsa_multi_r2_squarings(S)); }
+static_assert(rsa_log2_bits(64) == 11 && rsa_multi_r2_doublings(64) << rsa_multi_r2_squarings(64) == 2048, "R^2 schedule");
+template <int S>
+struct MultiR2 {   // the same, as compile-time constants usable in device code
+    static constexpr int SQ = rsa_multi_r2_squarings(S), KD = rsa_multi_r2_doublings(S);
+};
+
 // host-visible summary of a plan (also exported through the C-ABI)
 struct RsaPlanInfo {
     int width_class;              // S

@@ -740,9 +740,9 @@ int rsa_multi_plan_info(int nbits, int exp_bits, int mr, rsa_plan_info_t* info) 
     if (exp_bits < 1 || exp_bits > 32 * s_io) return RSA_ERANGE;
     const int w = multi_window(exp_bits);
     const int nwin = (exp_bits + w - 1) / w;
-    int K = 0;
-    while ((1 << K) < 32 * S) K++;
-    // modexp_multi.cu step machine: K SQR (R^2), 1 MUL (to Montgomery),
+    const int K = rsa_multi_r2_squarings(S);
+    // modexp_multi.cu step machine: K SQR (R^2, after rsa_multi_r2_doublings(S)
+    // modular doublings), 1 MUL (to Montgomery),
     // 2^w - 2 MUL (table), (nwin - 1) x (w SQR + 1 MUL) scan, then 1 MUL
     // (from Montgomery) or, for Miller-Rabin, r - 1 SQR (r ~ 1 on average)
     const long long sq = K + (long long)(nwin - 1) * w;
