@@ -1,6 +1,8 @@
 """The tensor-core Montgomery reduction on its own (csrc/mont_tc.cuh through
 csrc/microbench/tc_redc.cu, built with the library): for T = A B with A, B < n
-(random, and the extremes A = B = n - 1, A = 0, A = B = 1), the quotient
+(random, the extremes A = B = n - 1, A = 0, A = B = 1, and T constructed so that
+(T + m n) / R lands at n - d, n, n + d: the conditional subtraction's rare path
+where the top words tie and the full borrow chain decides), the quotient
 m = (T mod R) n' mod R read back from the staging buffer and the result
 U = T R^-1 mod n (canonical) are compared with Python integers, R = 2^2048,
 over a full persistent wave (148 x 256 packets, two tiles per CTA)."""

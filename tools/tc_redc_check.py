@@ -26,9 +26,19 @@ def main() -> int:
         if i % 7 == 0:      # extremes: A, B = n - 1, 0, 1
             a = [n - 1, 0, 1, n - 1][i // 7 % 4]
             b = [n - 1, n - 1, 1, 1][i // 7 % 4]
+            Ts.append(a * b)
+        elif i % 7 == 3:
+            # the subtraction's rare path: U' = (T + m n) / R placed at n - d, n or
+            # n + d (top word equal to n's: the full borrow chain decides).  With
+            # T = U' R - m n the kernel's own quotient (T mod R) n' mod R is m again.
+            d = [0, 1, 2, 1 << 40, (1 << 200) + 5][i // 7 % 5]
+            u = [n - d, n + d][i // 7 % 2] if d else n
+            m = rng.randrange(R // 4, R // 2)
+            Ts.append(u * R - m * n)
         else:
             a, b = rng.randrange(n), rng.randrange(n)
-        Ts.append(a * b)
+            Ts.append(a * b)
+    assert all(0 <= t < n * R for t in Ts)
     with open("in.bin", "wb") as f:
         f.write(struct.pack("<i", count))
         f.write(n.to_bytes(256, "little"))
