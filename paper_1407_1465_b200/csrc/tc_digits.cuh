@@ -3,10 +3,10 @@
 // exact DFMA.RZ split of mont_f64.cuh) streamed out as 32-bit words for the
 // tensor-core reduction (mont_tc.cuh), and the reduced words back to digits.
 //
-//   mul_scan:  T = A B by product scanning (column k = sum_{i+j=k} a_i b_j),
-//              each column's digit handed to put(k, d) as soon as it is final
-//              (f64::sqr_scan is the squaring counterpart: ND (ND+1)/2
-//              products instead of ND^2)
+//   mul_rows:  T = A B by rows, the loop rolled (the fully unrolled column
+//              scan of the first version was ~160 KB of SASS), the digits
+//              handed to put(k, d) in order (f64::sqr_col / sqr_scan are the
+//              squaring's column scans: ND (ND+1)/2 products instead of ND^2)
 //   Packer:    digit stream (52-bit digits in order) -> 32-bit words, each
 //              word handed to word(w, v) as soon as its 32 bits are in
 //   words_to_digits: 32-bit words -> 52-bit digits as doubles (A of the next op)
@@ -30,39 +30,8 @@ using f64::bits;
 using f64::fma_rz;
 using f64::sub_rn;
 
-// T = A B (2 ND digits), column by column.  b(j) returns digit j of B (a
-// double < 2^52).  Column k's sum: the low halves of its products, the high
-// halves of column k-1's (summed as they are produced), and the carry; every
-// term < 2^52 and at most 2 ND of them, so the 64-bit sums never overflow.
-template <int ND, typename BF, typename Put>
-__host__ __device__ __forceinline__ void mul_scan(const double (&a)[ND], BF b, Put put) {
-    uint64_t carry = 0, hprev = 0, hprevb = 0;
-#pragma unroll
-    for (int k = 0; k < 2 * ND; k++) {
-        uint64_t x = hprev, xb = hprevb, hs = 0, hsb = 0;
-#pragma unroll
-        for (int i = 0; i < ND; i++) {
-            const int j = k - i;
-            if (j >= 0 && j < ND) {
-                const double bj = b(j);
-                const double h = fma_rz(a[i], bj, C104);
-                const double l = fma_rz(a[i], bj, sub_rn(C2, h));
-                x += bits(l);
-                xb += BL;
-                hs += bits(h);
-                hsb += BH;
-            }
-        }
-        const uint64_t v = x - xb + carry;
-        carry = v >> D;
-        put(k, v & M52);
-        hprev = hs;
-        hprevb = hsb;
-    }
-}
-
 // T = A B by rows (operand scanning), the loop NOT unrolled (~40 products of
-// code instead of mul_scan's ND^2): iteration j adds a_i b_j to ND running
+// code instead of an unrolled ND^2 column scan): iteration j adds a_i b_j to ND running
 // 64-bit columns (low half to column j+i, high half to j+i+1), emits the
 // completed column j through lowout(j, digit), and shifts the columns down
 // by one in place (t[i-1] = t[i] + ...: CIOS's rename without the q n row).

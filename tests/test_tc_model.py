@@ -1,7 +1,7 @@
 """Design check, on CPU, of the CUDA-core half of the tensor-core Montgomery
 multiply (paper_1407_1465_b200/csrc/tc_digits.cuh, modexp_tc.cu): the product
 T = A B streamed out as 32-bit words (rolled row form mul_rows, the column
-scan mul_scan, the squaring's sqr_scan) and the word <-> 52-bit digit
+scans sqr_scan / sqr_col) and the word <-> 52-bit digit
 conversions, compiled for the host (tests/tools/tc_model.cu, rounding toward
 zero) and compared with Python integers.  The reduction half runs on the
 tensor core and is pinned on the GPU (tests/test_gpu_shapes.py, and the whole
@@ -50,11 +50,10 @@ def operands(rng):
         yield a & top, b & top
 
 
-@pytest.mark.parametrize("op", ["M", "C"])
-def test_product_words(model, op):
-    rng = random.Random(7 if op == "M" else 8)
+def test_product_words(model):
+    rng = random.Random(7)
     for a, b in operands(rng):
-        assert model(f"{op} {a:x} {b:x}") == a * b
+        assert model(f"M {a:x} {b:x}") == a * b
 
 
 @pytest.mark.parametrize("op", ["Q", "R"])

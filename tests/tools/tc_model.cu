@@ -7,7 +7,6 @@
 //   Q a     T = A^2 through sqr_scan + Packer
 //   R a     T = A^2 through sqr_col (compile-time-expanded scan, batch 2: the 2048-bit TC kernel)
 //   H a     the 1024-bit class (ND = 20, a < 2^1024): T = A^2 through sqr_col (batch 4), 64 words
-//   C a b   T = A B through mul_scan + Packer
 //   W x     x (64 words) -> 40 digits (words_to_digits) -> back to words (Packer)
 #include <cfenv>
 #include <cstdint>
@@ -74,8 +73,6 @@ int main() {
             double h[20];
             tcd::words_to_digits<20>([&](int w) -> uint32_t { return w < 32 ? aw[w] : 0u; }, h);
             f64::sqr_col<20, 0, 4, 0>(h, 0, 0, 0, put);
-        } else if (op == "C") {
-            tcd::mul_scan<ND>(a, [&](int j) { return b[j]; }, put);
         } else if (op == "W") {
             for (int k = 0; k < ND; k++) put(k, (uint64_t)a[k]);
             for (int k = ND; k < 2 * ND; k++) put(k, 0);
