@@ -55,6 +55,12 @@ namespace rsa_b200 {
 #ifndef RSA_TC_SQACC2
 #define RSA_TC_SQACC2 0     // two partial sums per column (A/B: 927K vs 953K at 2048 bits)
 #endif
+#ifndef RSA_TC_JOBS
+#define RSA_TC_JOBS 1       // 2048-bit: tile jobs (A/B at the 8-GPU slice: 897K vs 829K; 1M: 953K vs 947K)
+#endif
+#ifndef RSA_TC_JOBS32
+#define RSA_TC_JOBS32 0     // 1024-bit (4 tiles): thread mapping (A/B CRT-2048: 3.42M vs 3.35M with jobs)
+#endif
 #ifndef RSA_TC_LOCK32
 #define RSA_TC_LOCK32 0     // 1024-bit class: no CTA barrier per op (A/B: CRT-2048 3.44M vs 3.24M; its code is small)
 #endif
@@ -120,15 +126,18 @@ __global__ void __launch_bounds__(TcCfg<S>::BLOCK, 1) modexp_tc_kernel(const __g
     // one with one).  Every CTA runs the same trips; an idle tile still joins
     // the CTA barriers (lockstep), and a ragged job recomputes the batch's last
     // packet and skips the store.
+    // JOBS (RSA_TC_JOBS / RSA_TC_JOBS32): tile jobs as above; else packet =
+    // thread + trip x grid threads (every tile busy in every trip)
+    constexpr bool JOBS = (S == 64) ? RSA_TC_JOBS : RSA_TC_JOBS32;
     const unsigned long long slots = (unsigned long long)gridDim.x * C::TILES;
     const unsigned long long slot = (unsigned long long)tt.tile * gridDim.x + blockIdx.x;
     const unsigned long long jobs = (ip.count + tc::TILE - 1) / tc::TILE;
-    const unsigned long long trips = (jobs + slots - 1) / slots;
+    const unsigned long long trips = JOBS ? (jobs + slots - 1) / slots : (ip.count + nthr - 1) / nthr;
     for (unsigned long long tr = 0; tr < trips; tr++) {
         const unsigned long long job = slot + tr * slots;
-        const bool active = job < jobs;                  // uniform over the tile
-        if (__syncthreads_count(active) == 0) break;     // the whole CTA idle: done
-        const unsigned long long pkt0 = job * tc::TILE + tt.r;
+        const bool active = !JOBS || job < jobs;          // uniform over the tile
+        if (JOBS && __syncthreads_count(active) == 0) break;   // the whole CTA idle: done
+        const unsigned long long pkt0 = JOBS ? job * tc::TILE + tt.r : gtid + tr * nthr;
         const bool valid = active && pkt0 < ip.count;
         const unsigned long long pkt = valid ? pkt0 : ip.count - 1;
         const uint32_t* src = ip.base + pkt * (unsigned long long)ip.s_io;
