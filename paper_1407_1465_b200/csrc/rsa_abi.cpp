@@ -216,7 +216,7 @@ static void fill_tc(ModexpTcParams<S>* t, const BN& n) {
 }
 
 template <int S>
-static void fill_params(Plan& pl, const BN& n, const std::vector<RsaOp>& ops) {
+static bool fill_params(Plan& pl, const BN& n, const std::vector<RsaOp>& ops) {
     if constexpr (S == 64 || S == 32) {
         // FP64 params + the tensor-core kernel's n' (one blob serves every path of the class)
         pl.params.assign(sizeof(ModexpTcParams<S>), 0);
@@ -238,9 +238,10 @@ static void fill_params(Plan& pl, const BN& n, const std::vector<RsaOp>& ops) {
     rsa_host::to_limbs(r2, p->r2, S);
     for (size_t i = 0; i < ops.size(); i++) {
         // only squarings repeat (the kernels stage a multiply's operand once per op)
-        if (ops[i].kind != RSA_OP_SQR && ops[i].rep != 1) abort();
+        if (ops[i].kind != RSA_OP_SQR && ops[i].rep != 1) return false;
         p->ops[i] = ops[i];
     }
+    return true;
 }
 
 template <int S>
@@ -332,15 +333,17 @@ static int get_plan_ptr(const uint32_t* exp, const uint32_t* n, int nbits, std::
         }
         if (best < 0) return RSA_EINVAL;   // forced window does not fit
         pl.nops = (int)best_ops.size();
+        bool filled = false;
         switch (pl.S) {
-        case 2: fill_params<2>(pl, N, best_ops); break;
-        case 4: fill_params<4>(pl, N, best_ops); break;
-        case 8: fill_params<8>(pl, N, best_ops); break;
-        case 16: fill_params<16>(pl, N, best_ops); break;
-        case 32: fill_params<32>(pl, N, best_ops); break;
-        case 64: fill_params<64>(pl, N, best_ops); break;
-        case 128: fill_params<128>(pl, N, best_ops); break;
+        case 2: filled = fill_params<2>(pl, N, best_ops); break;
+        case 4: filled = fill_params<4>(pl, N, best_ops); break;
+        case 8: filled = fill_params<8>(pl, N, best_ops); break;
+        case 16: filled = fill_params<16>(pl, N, best_ops); break;
+        case 32: filled = fill_params<32>(pl, N, best_ops); break;
+        case 64: filled = fill_params<64>(pl, N, best_ops); break;
+        case 128: filled = fill_params<128>(pl, N, best_ops); break;
         }
+        if (!filled) return RSA_EINVAL;   // an op list the kernels cannot run (internal invariant)
     }
     auto sp = std::make_shared<const Plan>(std::move(pl));
     {
