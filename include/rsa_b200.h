@@ -221,8 +221,9 @@ typedef struct {
     long long digit_products; /* 52x52-bit digit products per packet on the FP64 pipe, each
                              2 DFMA + 1 DADD.  FP64 kernel: squarings x (ND(ND+1)/2 + ND^2) +
                              other montmuls x 2 ND^2.  Tensor-core path (RSA_PATH_TC): the
-                             product T = A B only, squarings x ND(ND+1)/2 + other montmuls x
-                             ND^2 (the reduction runs on the tensor core).  0 for
+                             product T = A B only, squarings x ND(ND+1)/2 (x ND^2 at S = 128,
+                             sqr_kernel 0) + other montmuls x ND^2 (the reduction runs on the
+                             tensor core).  0 for
                              integer-pipe classes */
 } rsa_plan_info_t;
 
@@ -245,18 +246,17 @@ int rsa_set_window(int w);
  * thread shape differ.  Paths:
  *   RSA_PATH_DEFAULT    the measured default of the class (see below)
  *   RSA_PATH_FP64       S = 32, 64, 128: 52-bit digits on the FP64 pipe
- *                       (default for S = 128)
  *   RSA_PATH_INT        32-bit limbs, IMAD carry chains, one thread per packet
  *                       (default for S = 8, 16; for S = 128 it means the
  *                       2-lane pair kernel)
  *   RSA_PATH_INT_GROUP  S = 64: 2 lanes per packet; S = 128: 4 lanes
  *   RSA_PATH_INT_PAIR   S = 128: 2 lanes per packet
  *   RSA_PATH_INT_MULTI  S = 2, 4: several packets per thread (default there)
- *   RSA_PATH_TC         S = 32, 64: the product A B on the FP64 pipe, the
- *                       Montgomery reduction (m = T n' mod R, T + m n) as u8
- *                       matrix products on the tensor core (tcgen05, TMEM),
+ *   RSA_PATH_TC         S = 32, 64, 128: the product A B on the FP64 pipe,
+ *                       the Montgomery reduction (m = T n' mod R, T + m n) as
+ *                       u8 matrix products on the tensor core (tcgen05, TMEM),
  *                       R = 2^(32 S); 128-packet tiles, one CTA per SM
- *                       (default for S = 32, 64)
+ *                       (default for S = 32, 64, 128)
  * rsa_set_kernel_path sets the path of class `width_class` for subsequent
  * calls of every thread (process-wide, thread-safe; a call in flight keeps the
  * path it started with).  RSA_PATH_DEFAULT restores the default, under which

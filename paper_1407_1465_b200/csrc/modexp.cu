@@ -784,7 +784,7 @@ int rsa_b200_path_valid(int S, int path) {
     case RSA_PATH_INT_GROUP: return S == 64 || S == 128;
     case RSA_PATH_INT_PAIR: return S == 128;
     case RSA_PATH_INT_MULTI: return S <= 4;
-    case RSA_PATH_TC: return S == 32 || S == 64;
+    case RSA_PATH_TC: return S == 32 || S == 64 || S == 128;
     default: return 0;
     }
 }
@@ -815,7 +815,7 @@ int rsa_b200_resolve_path(int S) {
         else
             p = (env_is("RSA_B200_F64", '0') || env_is("RSA_B200_F64_4096", '0'))
                     ? (env_is("RSA_B200_TPI128", '4') ? RSA_PATH_INT_GROUP : RSA_PATH_INT_PAIR)
-                    : RSA_PATH_FP64;
+                    : env_is("RSA_B200_TC", '0') ? RSA_PATH_FP64 : RSA_PATH_TC;
     }
     if (S == 128 && p == RSA_PATH_INT) p = RSA_PATH_INT_PAIR;
     if (S > 4 && p == RSA_PATH_INT_MULTI) p = RSA_PATH_INT;
@@ -831,9 +831,10 @@ int rsa_b200_resolve_path(int S) {
 // kernel have no squaring path.  Used for the window choice and the
 // executed-product count of rsa_plan_info.
 int rsa_b200_f64_sqr(int S);
+int rsa_b200_tc_sqr(int S);
 int rsa_b200_sqr_dedicated(int S, int path) {
     if (path == RSA_PATH_FP64) return rsa_b200_f64_sqr(S);
-    if (path == RSA_PATH_TC) return 1;
+    if (path == RSA_PATH_TC) return rsa_b200_tc_sqr(S);
     return (path == RSA_PATH_INT && S <= 64) ? 1 : 0;
 }
 

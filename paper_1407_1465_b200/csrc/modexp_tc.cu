@@ -61,6 +61,16 @@ namespace rsa_b200 {
 #ifndef RSA_TC_JOBS32
 #define RSA_TC_JOBS32 0     // 1024-bit (4 tiles): thread mapping (A/B CRT-2048: 3.42M vs 3.35M with jobs)
 #endif
+#ifndef RSA_TC_SQB128
+#define RSA_TC_SQB128 4     // 4096-bit squaring scan batch (the FP64 kernel's measured best at ND = 80)
+#endif
+#ifndef RSA_TC_SQROWS128
+#define RSA_TC_SQROWS128 1  // 4096-bit squarings by the rolled row form: ND^2 = 6400 digit products instead
+#endif                      // of 3240, but a few KB of code: A/B 70.4K vs 57.8K decrypts/s (the ~300 KB
+                            // expanded scan starves on instruction fetch at 4 warps/SM: no_instruction 2.2)
+#ifndef RSA_TC_APAIR
+#define RSA_TC_APAIR 0      // 4096-bit A slot as digit pairs (A/B)
+#endif
 #ifndef RSA_TC_LOCK32
 #define RSA_TC_LOCK32 0     // 1024-bit class: no CTA barrier per op (A/B: CRT-2048 3.44M vs 3.24M; its code is small)
 #endif
@@ -74,8 +84,13 @@ namespace rsa_b200 {
 template <int S>
 struct TcCfg {
     static constexpr int KB = 4 * S;
-    static constexpr int ND = rsa_f64_digits(S);      // 40 at S = 64, 20 at S = 32
-    static constexpr int TILES = (S == 64) ? 2 : RSA_TC_TILES32;
+    static constexpr int ND = rsa_f64_digits(S);      // 40 at S = 64, 20 at S = 32, 80 at S = 128
+    static constexpr int TILES = (S == 64) ? 2 : (S == 128 ? 1 : RSA_TC_TILES32);
+    // S = 128: one tile (512 TMEM columns); A lives in the thread's shared-memory
+    // slot between ops (registers: the square's 160 for A, or the row-form
+    // multiply's 80 columns), the multiply's B is read in place
+    static constexpr bool SLOTA = (S == 128);
+    static constexpr bool LOCK = (S == 64) ? RSA_TC_LOCK : (S == 32 ? RSA_TC_LOCK32 : 0);
     static constexpr int BLOCK = TILES * tc::TILE;
     static constexpr int TMEM_COLS = (KB * TILES <= 256) ? 256 : 512;
     static_assert(KB * TILES <= 512, "TMEM: KB columns per tile");
@@ -128,7 +143,7 @@ __global__ void __launch_bounds__(TcCfg<S>::BLOCK, 1) modexp_tc_kernel(const __g
     // packet and skips the store.
     // JOBS (RSA_TC_JOBS / RSA_TC_JOBS32): tile jobs as above; else packet =
     // thread + trip x grid threads (every tile busy in every trip)
-    constexpr bool JOBS = (S == 64) ? RSA_TC_JOBS : RSA_TC_JOBS32;
+    constexpr bool JOBS = (S == 64) ? RSA_TC_JOBS : (S == 32 ? RSA_TC_JOBS32 : 0);
     const unsigned long long slots = (unsigned long long)gridDim.x * C::TILES;
     const unsigned long long slot = (unsigned long long)tt.tile * gridDim.x + blockIdx.x;
     const unsigned long long jobs = (ip.count + tc::TILE - 1) / tc::TILE;
@@ -157,14 +172,51 @@ __global__ void __launch_bounds__(TcCfg<S>::BLOCK, 1) modexp_tc_kernel(const __g
         };
         double a[ND];
         uint32_t th[NW];
+        // SLOTA: A's digits in the thread's slot, digit-major (stride TC_BLOCK) or, with
+        // RSA_TC_APAIR, as digit pairs (digit k at pair k/2, 16 bytes per thread per pair)
+        double* const aslot = RSA_TC_APAIR ? reinterpret_cast<double*>(smem_raw + sizeof(Shared)) + 2 * threadIdx.x
+                                           : bslot;
+        auto slot_at = [&](int k) -> double* {
+            if constexpr (RSA_TC_APAIR != 0) return aslot + (k >> 1) * 2 * TC_BLOCK + (k & 1);
+            else return aslot + k * TC_BLOCK;
+        };
+        auto set_digit = [&](int k, double v) {
+            if constexpr (C::SLOTA) *slot_at(k) = v;
+            else a[k] = v;
+        };
+        auto get_digit = [&](int k) -> double {
+            if constexpr (C::SLOTA) return f64::ld_digit(slot_at(k));
+            else return a[k];
+        };
+        // the row loop's A: two digits per 128-bit load when paired
+        double apair_hi = 0.0;
+        auto get_digit_rows = [&](int k) -> double {
+            if constexpr (C::SLOTA && RSA_TC_APAIR != 0) {
+                if ((k & 1) == 0) {
+                    double x;
+                    f64::nd_pair(slot_at(k), 0, x, apair_hi);
+                    return x;
+                }
+                return apair_hi;
+            } else {
+                return get_digit(k);
+            }
+        };
         if (!active) {
             // an idle tile in a partial trip: only the CTA barriers of the busy one
-            if constexpr ((S == 64 ? RSA_TC_LOCK : RSA_TC_LOCK32) != 0)
+            if constexpr (C::LOCK)
                 for (int i = 0; i < ip.nops; i++)
                     for (int r = 0; r < ip.ops[i].rep; r++) __syncthreads();
             continue;
         }
-        load_input(a);
+        if constexpr (C::SLOTA) {
+            double x[ND];
+            load_input(x);
+#pragma unroll
+            for (int k = 0; k < ND; k++) set_digit(k, x[k]);
+        } else {
+            load_input(a);
+        }
 
         for (int i = 0; i < ip.nops; i++) {
             const RsaOp op = ip.ops[i];
@@ -172,14 +224,16 @@ __global__ void __launch_bounds__(TcCfg<S>::BLOCK, 1) modexp_tc_kernel(const __g
 #pragma unroll
                 for (int g = 0; g < NP; g++) {
                     const double2 v = table[((size_t)op.lidx * NP + g) * nthr + gtid];
-                    a[2 * g] = v.x;
-                    a[2 * g + 1] = v.y;
+                    set_digit(2 * g, v.x);
+                    set_digit(2 * g + 1, v.y);
                 }
             }
             // the second operand of a multiply goes to this thread's slot (once per op: only
             // squarings repeat, rep > 1; the plan builder guarantees rep == 1 for the others,
             // whose row-form product overwrites the slot with T's low digits)
-            if (op.kind == RSA_OP_MUL) {
+            if (C::SLOTA) {
+                // (S = 128: B is read in place by the row-form multiply)
+            } else if (op.kind == RSA_OP_MUL) {
 #pragma unroll
                 for (int g = 0; g < NP; g++) {
                     const double2 v = table[((size_t)op.bidx * NP + g) * nthr + gtid];
@@ -199,7 +253,7 @@ __global__ void __launch_bounds__(TcCfg<S>::BLOCK, 1) modexp_tc_kernel(const __g
                 for (int k = 0; k < ND; k++) bslot[k * TC_BLOCK] = (k == 0) ? 1.0 : 0.0;
             }
             for (int r = 0; r < op.rep; r++) {
-                if constexpr ((S == 64 ? RSA_TC_LOCK : RSA_TC_LOCK32) != 0) __syncthreads();   // all tiles on the same code lines
+                if constexpr (C::LOCK) __syncthreads();   // all tiles on the same code lines
                 // T = A B: words 0..63 to the staging buffer (16-byte chunks), 64..127 to th
                 uint32_t t63 = 0, wb0 = 0, wb1 = 0, wb2 = 0;
                 auto word = [&](int w, uint32_t v) {
@@ -215,13 +269,61 @@ __global__ void __launch_bounds__(TcCfg<S>::BLOCK, 1) modexp_tc_kernel(const __g
                 };
                 tcd::Packer<2 * NW, decltype(word)> pk{word, 0};
                 auto put = [&](int k, uint64_t d) { pk.put(k, d); };
-                if (op.kind == RSA_OP_SQR) {
-                    if constexpr ((S == 32 && RSA_TC_SQREC32) || (S == 64 && RSA_TC_SQREC64))
+                if (op.kind == RSA_OP_SQR && !(C::SLOTA && RSA_TC_SQROWS128)) {
+                    if constexpr (C::SLOTA) {
+#pragma unroll
+                        for (int k = 0; k < ND; k++) a[k] = get_digit(k);
+                        f64::sqr_col<ND, 0, RSA_TC_SQB128, 0>(a, 0, 0, 0, put);
+                    } else if constexpr ((S == 32 && RSA_TC_SQREC32) || (S == 64 && RSA_TC_SQREC64))
                         // the compile-time-expanded scan (the loop form is not unrolled at ND = 20
                         // here; at ND = 40, A/B: 949K vs 901K decrypts/s)
                         f64::sqr_col<ND, 0, (S == 64 ? RSA_TC_SQB64 : RSA_TC_SQB32), RSA_TC_SQACC2>(a, 0, 0, 0, put);
                     else
                         f64::sqr_scan<ND>(a, put);
+                } else if constexpr (C::SLOTA) {
+                    // rows with A read from its slot and B in place (table / R^2 / 1);
+                    // T's low digits leave as words at run time: words 0 .. NW-1 to the
+                    // staging buffer, NW and NW+1 (digit ND-1's top bits) to th
+                    auto bget = [&](int j) -> double {
+                        if (op.kind == RSA_OP_SQR) return get_digit(j);   // RSA_TC_SQROWS128: A A by rows
+                        if (op.kind == RSA_OP_MUL) {
+                            const double2 v = table[((size_t)op.bidx * NP + (j >> 1)) * nthr + gtid];
+                            return (j & 1) ? v.y : v.x;
+                        }
+                        if (op.kind == RSA_OP_R2) return r2d[j];
+                        return j == 0 ? 1.0 : 0.0;                   // RSA_OP_ONE (no MULX at S = 128)
+                    };
+                    uint64_t eacc = 0;
+                    int enb = 0, ew = 0;
+                    auto emit = [&](uint32_t v) {
+                        if (ew < NW) {
+                            reinterpret_cast<uint32_t*>(sh.stage[tt.tile] + (ew >> 2) * tc::STAGE_LBO +
+                                                        tt.r * 16)[ew & 3] = v;
+                            if (ew == NW - 1) t63 = v;
+                        } else if (ew == NW) {
+                            th[0] = v;
+                        } else {
+                            th[1] = v;
+                        }
+                        ew++;
+                    };
+                    // digit d (52 bits) joins the enb < 32 pending bits; whole words leave
+                    auto lout = [&](int, uint64_t d) {
+                        const uint64_t lo64 = eacc | (d << enb);
+                        const uint64_t hi = enb > 12 ? (d >> (64 - enb)) : 0;
+                        emit((uint32_t)lo64);
+                        uint64_t rest = (lo64 >> 32) | (hi << 32);
+                        int nb = enb + 20;
+                        if (nb >= 32) {
+                            emit((uint32_t)rest);
+                            rest >>= 32;
+                            nb -= 32;
+                        }
+                        eacc = rest;
+                        enb = nb;
+                    };
+                    auto lin = [&](int) -> uint64_t { return 0; };
+                    tcd::mul_rows_f<ND, false>(get_digit_rows, bget, lout, lin, put);
                 } else {
                     // rows, rolled (the unrolled column scan is ~160 KB of code);
                     // T's low digits go back into b's slot as b's digits are used up
@@ -231,12 +333,12 @@ __global__ void __launch_bounds__(TcCfg<S>::BLOCK, 1) modexp_tc_kernel(const __g
                     tcd::mul_rows<ND>(a, bget, lout, lin, put);
                 }
                 tc::redc(sh, tt, t63, th);
-                tcd::words_to_digits<ND>([&](int w) -> uint32_t { return w < NW ? th[w] : 0u; }, a);
+                tcd::words_to_digits_f<ND>([&](int w) -> uint32_t { return w < NW ? th[w] : 0u; }, set_digit);
             }
             if (op.flags & RSA_F_STORE) {
 #pragma unroll
                 for (int g = 0; g < NP; g++)
-                    table[((size_t)op.sidx * NP + g) * nthr + gtid] = make_double2(a[2 * g], a[2 * g + 1]);
+                    table[((size_t)op.sidx * NP + g) * nthr + gtid] = make_double2(get_digit(2 * g), get_digit(2 * g + 1));
             }
         }
         // the last op (RSA_OP_ONE or RSA_OP_MULX) left the canonical result in th
@@ -292,11 +394,16 @@ static cudaError_t launch_tc(const void* params, int sms, cudaStream_t stream, i
 
 }  // namespace rsa_b200
 
+// 1 if class S's squarings run a dedicated squaring (ND (ND+1)/2 digit products on
+// the CUDA cores), 0 if the row-form product (ND^2)
+int rsa_b200_tc_sqr(int S) { return (S == 128 && RSA_TC_SQROWS128) ? 0 : 1; }
+
 cudaError_t rsa_b200_launch_tc(int S, const void* params, int sms, cudaStream_t stream, int* grid, int* block,
                                size_t* slots, bool query_only) {
     switch (S) {
     case 32: return rsa_b200::launch_tc<32>(params, sms, stream, grid, block, slots, query_only);
     case 64: return rsa_b200::launch_tc<64>(params, sms, stream, grid, block, slots, query_only);
+    case 128: return rsa_b200::launch_tc<128>(params, sms, stream, grid, block, slots, query_only);
     default: return cudaErrorInvalidValue;
     }
 }

@@ -52,8 +52,9 @@ struct Geom {
     static constexpr int G2_C0 = KB - 4;
     static constexpr int N_RHO0 = G2_C0 - (KB - 32), N_ROWS = 2 * KB - 32, N_LBO = N_ROWS * 16;
     static constexpr int NP_STRIP_BYTES = 2 * NP_LBO, N_STRIP_BYTES = 2 * N_LBO;
-    static constexpr int G2_N = KB < 256 ? KB : 256;          // MMA N of GEMM2 (one N block per K block)
-    static_assert(KB == 128 || KB == 256, "one GEMM2 N block");
+    static constexpr int G2_N = KB < 256 ? KB : 256;          // MMA N of GEMM2
+    static constexpr int G2_NB = KB / G2_N;                   // GEMM2 N blocks per K block (2 at KB = 512)
+    static_assert(KB == 128 || KB == 256 || KB == 512, "operand widths of the TC kernels");
 };
 
 template <int KB, int TILES>
@@ -109,17 +110,20 @@ __device__ __forceinline__ void issue_gemm1(TcShared<KB, TILES>& sh, int tile, u
     }
 }
 
-// GEMM2 (columns G2_C0 .. G2_C0 + KB - 1 of m n): one N = KB block per K block
+// GEMM2 (columns G2_C0 .. G2_C0 + KB - 1 of m n): KB / G2_N blocks of N = G2_N per K block
 template <int KB, int TILES>
 __device__ __forceinline__ void issue_gemm2(TcShared<KB, TILES>& sh, int tile, uint32_t tmem) {
     using G = Geom<KB>;
     const uint32_t st = smem_u32(sh.stage[tile]), sn = smem_u32(sh.n_strip);
     constexpr uint32_t id = idesc_u8(128, G::G2_N);
 #pragma unroll
-    for (int I = 0; I < KB / 32; I++) {
-        const uint64_t a = sdesc(st + 2 * I * STAGE_LBO, STAGE_LBO, 128);
-        const uint64_t b = sdesc(sn + (G::G2_C0 - 32 * I - G::N_RHO0) * 16, G::N_LBO, 128);
-        mma_u8(tmem, a, b, id, I > 0);
+    for (int h = 0; h < G::G2_NB; h++) {
+#pragma unroll
+        for (int I = 0; I < KB / 32; I++) {
+            const uint64_t a = sdesc(st + 2 * I * STAGE_LBO, STAGE_LBO, 128);
+            const uint64_t b = sdesc(sn + (G::G2_C0 + G::G2_N * h - 32 * I - G::N_RHO0) * 16, G::N_LBO, 128);
+            mma_u8(tmem + G::G2_N * h, a, b, id, I > 0);
+        }
     }
 }
 

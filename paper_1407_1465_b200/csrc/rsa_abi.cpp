@@ -217,14 +217,11 @@ static void fill_tc(ModexpTcParams<S>* t, const BN& n) {
 
 template <int S>
 static bool fill_params(Plan& pl, const BN& n, const std::vector<RsaOp>& ops) {
-    if constexpr (S == 64 || S == 32) {
+    if constexpr (S == 64 || S == 32 || S == 128) {
         // FP64 params + the tensor-core kernel's n' (one blob serves every path of the class)
         pl.params.assign(sizeof(ModexpTcParams<S>), 0);
         fill_f64<S>(reinterpret_cast<ModexpF64Params<S>*>(pl.params.data()), n);
         if (pl.path == RSA_PATH_TC) fill_tc<S>(reinterpret_cast<ModexpTcParams<S>*>(pl.params.data()), n);
-    } else if constexpr (S == 128) {
-        pl.params.assign(sizeof(ModexpF64Params<S>), 0);
-        fill_f64<S>(reinterpret_cast<ModexpF64Params<S>*>(pl.params.data()), n);
     } else {
         pl.params.assign(sizeof(ModexpParams<S>), 0);
     }
@@ -314,7 +311,7 @@ static int get_plan_ptr(const uint32_t* exp, const uint32_t* n, int nbits, std::
             int ntab;
             long long mm, sq;
             // the 4096-bit FP64 kernel has one shared-memory slot (A): no raw-input multiply
-            const bool mulx = !(pl.S == 128 && pl.path == RSA_PATH_FP64);
+            const bool mulx = !(pl.S == 128 && (pl.path == RSA_PATH_FP64 || pl.path == RSA_PATH_TC));
             if (!build_ops(E, w, rsa_ops_cap(pl.S), &ops, &ntab, &mm, &sq, mulx)) continue;
             // minimise executed limb products (squarings are cheaper when the
             // class has the dedicated squaring kernel)
@@ -696,7 +693,8 @@ int rsa_plan_info(const uint32_t* exp, const uint32_t* n, int nbits, rsa_plan_in
         // byte products run on the tensor core
         const long long nd = rsa_f64_digits(pl.S);
         info->fp64_digits = (int)nd;
-        info->digit_products = pl.squarings * (nd * (nd + 1) / 2) + (pl.montmuls - pl.squarings) * nd * nd;
+        info->digit_products = pl.squarings * (info->sqr_kernel ? nd * (nd + 1) / 2 : nd * nd) +
+                               (pl.montmuls - pl.squarings) * nd * nd;
     }
     const int sms = device_sms();
     if (sms) {

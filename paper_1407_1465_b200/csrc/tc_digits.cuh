@@ -39,8 +39,11 @@ using f64::sub_rn;
 // the loop the low digits are replayed into put in order (lowin(k) returns
 // what lowout(k) stored), then the high columns are normalised into put.
 // Column bounds: <= 2 terms < 2^52 per column per iteration, <= ND iterations.
-template <int ND, typename BF, typename LO, typename LI, typename Put>
-__host__ __device__ __forceinline__ void mul_rows(const double (&a)[ND], BF b, LO lowout, LI lowin, Put put) {
+// mul_rows_f: the same with A read through a(i) (registers, or the thread's
+// shared-memory slot at 4096 bits) and, for REPLAY = false, no replay of the
+// low digits (lowout then consumes them, e.g. as words written at run time).
+template <int ND, bool REPLAY, typename AF, typename BF, typename LO, typename LI, typename Put>
+__host__ __device__ __forceinline__ void mul_rows_f(AF a, BF b, LO lowout, LI lowin, Put put) {
     uint64_t t[ND];
 #pragma unroll
     for (int i = 0; i < ND; i++) t[i] = 0;
@@ -51,16 +54,18 @@ __host__ __device__ __forceinline__ void mul_rows(const double (&a)[ND], BF b, L
 #endif
     for (int j = 0; j < ND; j++) {
         const double bn = b(j + 1 < ND ? j + 1 : j);
-        const double h0 = fma_rz(a[0], bj, C104);
-        const double l0 = fma_rz(a[0], bj, sub_rn(C2, h0));
+        const double a0 = a(0);
+        const double h0 = fma_rz(a0, bj, C104);
+        const double l0 = fma_rz(a0, bj, sub_rn(C2, h0));
         const uint64_t v = t[0] + bits(l0) - bias + carry;   // column j: (j+1) lows, j highs
         carry = v >> D;
         lowout(j, v & M52);
         uint64_t hp = bits(h0);
 #pragma unroll
         for (int i = 1; i < ND; i++) {
-            const double h = fma_rz(a[i], bj, C104);
-            const double l = fma_rz(a[i], bj, sub_rn(C2, h));
+            const double ai = a(i);
+            const double h = fma_rz(ai, bj, C104);
+            const double l = fma_rz(ai, bj, sub_rn(C2, h));
             t[i - 1] = t[i] + bits(l) + hp;
             hp = bits(h);
         }
@@ -68,8 +73,10 @@ __host__ __device__ __forceinline__ void mul_rows(const double (&a)[ND], BF b, L
         bias += BL + BH;
         bj = bn;
     }
+    if constexpr (REPLAY) {
 #pragma unroll
-    for (int k = 0; k < ND; k++) put(k, lowin(k));
+        for (int k = 0; k < ND; k++) put(k, lowin(k));
+    }
     // t[p] = column ND + p: (ND-1-p) lows, (ND-p) highs
 #pragma unroll
     for (int p = 0; p < ND; p++) {
@@ -77,6 +84,11 @@ __host__ __device__ __forceinline__ void mul_rows(const double (&a)[ND], BF b, L
         carry = v >> D;
         put(ND + p, v & M52);
     }
+}
+
+template <int ND, typename BF, typename LO, typename LI, typename Put>
+__host__ __device__ __forceinline__ void mul_rows(const double (&a)[ND], BF b, LO lowout, LI lowin, Put put) {
+    mul_rows_f<ND, true>([&](int i) -> double { return a[i]; }, b, lowout, lowin, put);
 }
 
 // digit stream -> 32-bit words (words 0 .. NWORDS-1; bits beyond are dropped).
@@ -99,16 +111,22 @@ struct Packer {
     }
 };
 
-// words (w(i) = word i, 0 beyond the number) -> ND digits of 52 bits as doubles
-template <int ND, typename WF>
-__host__ __device__ __forceinline__ void words_to_digits(WF wd, double (&a)[ND]) {
+// words (w(i) = word i, 0 beyond the number) -> ND digits of 52 bits as
+// doubles, handed to out(k, digit) (words_to_digits: into an array)
+template <int ND, typename WF, typename OF>
+__host__ __device__ __forceinline__ void words_to_digits_f(WF wd, OF out) {
 #pragma unroll
     for (int k = 0; k < ND; k++) {
         const int o = D * k, w0 = o / 32, sh = o % 32;
         uint64_t v = ((uint64_t)wd(w0) >> sh) | ((uint64_t)wd(w0 + 1) << (32 - sh));
         if (sh > 12) v |= (uint64_t)wd(w0 + 2) << (64 - sh);
-        a[k] = f64::digit_to_double(v & M52);
+        out(k, f64::digit_to_double(v & M52));
     }
+}
+
+template <int ND, typename WF>
+__host__ __device__ __forceinline__ void words_to_digits(WF wd, double (&a)[ND]) {
+    words_to_digits_f<ND>(wd, [&](int k, double v) { a[k] = v; });
 }
 
 }  // namespace tcd

@@ -103,11 +103,11 @@ def test_kernel_path_knob():
     import paper_1407_1465_b200 as R
     import workload
     defaults = {2: R.RSA_PATH_INT_MULTI, 4: R.RSA_PATH_INT_MULTI, 8: R.RSA_PATH_INT, 16: R.RSA_PATH_INT,
-                32: R.RSA_PATH_TC, 64: R.RSA_PATH_TC, 128: R.RSA_PATH_FP64}
+                32: R.RSA_PATH_TC, 64: R.RSA_PATH_TC, 128: R.RSA_PATH_TC}
     for S, p in defaults.items():
         assert R.rsa_get_kernel_path(S) == p, S
     for S, p in [(8, R.RSA_PATH_FP64), (64, R.RSA_PATH_INT_PAIR), (128, R.RSA_PATH_INT_MULTI), (3, 0), (64, 9),
-                 (16, R.RSA_PATH_TC), (128, R.RSA_PATH_TC)]:
+                 (16, R.RSA_PATH_TC), (8, R.RSA_PATH_TC)]:
         with pytest.raises(R.RsaError):
             R.rsa_set_kernel_path(S, p)
     with pytest.raises(R.RsaError):

@@ -41,7 +41,8 @@ def moduli(nb):
 
 @pytest.mark.parametrize("nb,path", [(513, None), (1000, None), (1024, None), (1025, None), (1536, None),
                                      (2047, None), (2048, None), (2049, None), (3072, None), (4095, None),
-                                     (4096, None), (1024, "FP64"), (2048, "FP64"), (1025, "FP64")])
+                                     (4096, None), (1024, "FP64"), (2048, "FP64"), (1025, "FP64"),
+                                     (4096, "FP64"), (3072, "FP64")])
 def test_f64_edge_moduli(R, nb, path):
     if path is None:
         _edges(R, nb)

@@ -40,7 +40,7 @@ def _classes(key):
     return next(c for c in (2, 4, 8, 16, 32, 64, 128) if s <= c)
 
 
-@pytest.mark.parametrize("path,key,count", [("TC", "rsa2048", 300), ("TC", "rsa1536", 300), ("TC", "rsa1024", 700),
+@pytest.mark.parametrize("path,key,count", [("TC", "rsa4096", 60), ("TC", "rsa3072", 60), ("TC", "rsa2048", 300), ("TC", "rsa1536", 300), ("TC", "rsa1024", 700),
                                             ("TC", "rsa1000", 300), ("TC", "rsa768", 300),
                                             ("INT", "rsa2048", 300), ("INT", "rsa1536", 300),
                                             ("INT", "rsa1024", 300), ("FP64", "rsa1024", 300),
