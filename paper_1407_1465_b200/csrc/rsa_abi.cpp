@@ -234,8 +234,12 @@ static bool fill_params(Plan& pl, const BN& n, const std::vector<RsaOp>& ops) {
     BN r2 = rsa_host::pow2_mod(64 * S, n);      // R^2 mod n, R = 2^(32 S)
     rsa_host::to_limbs(r2, p->r2, S);
     for (size_t i = 0; i < ops.size(); i++) {
-        // only squarings repeat (the kernels stage a multiply's operand once per op)
+        // only squarings repeat (the kernels stage a multiply's operand once per op);
+        // the 4096-bit kernels have no slot for a raw-input multiply (RSA_OP_MULX)
         if (ops[i].kind != RSA_OP_SQR && ops[i].rep != 1) return false;
+        if (S == 128 && ops[i].kind == RSA_OP_MULX && pl.path != RSA_PATH_INT_PAIR &&
+            pl.path != RSA_PATH_INT_GROUP)
+            return false;
         p->ops[i] = ops[i];
     }
     return true;
