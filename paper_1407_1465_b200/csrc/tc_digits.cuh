@@ -42,8 +42,14 @@ using f64::sub_rn;
 // mul_rows_f: the same with A read through a(i) (registers, or the thread's
 // shared-memory slot at 4096 bits) and, for REPLAY = false, no replay of the
 // low digits (lowout then consumes them, e.g. as words written at run time).
-template <int ND, bool REPLAY, typename AF, typename BF, typename LO, typename LI, typename Put>
+//
+// NR < ND rows (b(0 .. NR-1)) give the partial product A (b_0 .. b_{NR-1}):
+// lowout receives its columns 0 .. NR-1, put its columns NR .. NR+ND-1
+// (model-tested; a split of one product's rows over two threads was measured
+// slower at 4096 bits, profiles/r02_ab_summary.md).
+template <int ND, bool REPLAY, typename AF, typename BF, typename LO, typename LI, typename Put, int NR = ND>
 __host__ __device__ __forceinline__ void mul_rows_f(AF a, BF b, LO lowout, LI lowin, Put put) {
+    static_assert(NR >= 1 && NR <= ND, "rows");
     uint64_t t[ND];
 #pragma unroll
     for (int i = 0; i < ND; i++) t[i] = 0;
@@ -52,8 +58,8 @@ __host__ __device__ __forceinline__ void mul_rows_f(AF a, BF b, LO lowout, LI lo
 #ifdef __CUDA_ARCH__
 #pragma unroll 1
 #endif
-    for (int j = 0; j < ND; j++) {
-        const double bn = b(j + 1 < ND ? j + 1 : j);
+    for (int j = 0; j < NR; j++) {
+        const double bn = b(j + 1 < NR ? j + 1 : j);
         const double a0 = a(0);
         const double h0 = fma_rz(a0, bj, C104);
         const double l0 = fma_rz(a0, bj, sub_rn(C2, h0));
@@ -75,14 +81,15 @@ __host__ __device__ __forceinline__ void mul_rows_f(AF a, BF b, LO lowout, LI lo
     }
     if constexpr (REPLAY) {
 #pragma unroll
-        for (int k = 0; k < ND; k++) put(k, lowin(k));
+        for (int k = 0; k < NR; k++) put(k, lowin(k));
     }
-    // t[p] = column ND + p: (ND-1-p) lows, (ND-p) highs
+    // t[p] = column NR + p: min(NR, ND-1-p) lows, min(NR, ND-p) highs
 #pragma unroll
     for (int p = 0; p < ND; p++) {
-        const uint64_t v = t[p] - ((uint64_t)(ND - 1 - p) * BL + (uint64_t)(ND - p) * BH) + carry;
+        const uint64_t nl = (NR < ND - 1 - p) ? NR : ND - 1 - p, nh = (NR < ND - p) ? NR : ND - p;
+        const uint64_t v = t[p] - (nl * BL + nh * BH) + carry;
         carry = v >> D;
-        put(ND + p, v & M52);
+        put(NR + p, v & M52);
     }
 }
 

@@ -63,6 +63,13 @@ def test_square_words(model, op):
         assert model(f"{op} {a:x}") == a * a
 
 
+def test_product_split_rows(model):
+    """mul_rows_f with NR < ND rows: the two row halves of one product, summed."""
+    rng = random.Random(12)
+    for a, b in operands(rng):
+        assert model(f"P {a:x} {b:x}") == a * b
+
+
 def test_square_words_1024(model):
     rng = random.Random(11)
     for a, _ in operands(rng):

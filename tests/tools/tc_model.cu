@@ -8,6 +8,7 @@
 //   R a     T = A^2 through sqr_col (compile-time-expanded scan, batch 2: the 2048-bit TC kernel)
 //   H a     the 1024-bit class (ND = 20, a < 2^1024): T = A^2 through sqr_col (batch 4), 64 words
 //   W x     x (64 words) -> 40 digits (words_to_digits) -> back to words (Packer)
+//   P a b   A B as two row halves (mul_rows_f with NR = 20 on b_0..19 and b_20..39), summed
 #include <cfenv>
 #include <cstdint>
 #include <cstdio>
@@ -73,6 +74,28 @@ int main() {
             double h[20];
             tcd::words_to_digits<20>([&](int w) -> uint32_t { return w < 32 ? aw[w] : 0u; }, h);
             f64::sqr_col<20, 0, 4, 0>(h, 0, 0, 0, put);
+        } else if (op == "P") {
+            // rows split in two: P0 = A (b_0..b_19), P1 = A (b_20..b_39); T = P0 + P1 2^(52 * 20)
+            constexpr int NR = 20;
+            uint64_t dig[2][ND + NR];
+            for (int hf = 0; hf < 2; hf++) {
+                auto ag = [&](int i) { return a[i]; };
+                auto bg = [&](int j) { return b[hf * NR + j]; };
+                auto lo = [&](int j, uint64_t d) { dig[hf][j] = d; };
+                auto li = [&](int) -> uint64_t { return 0; };
+                auto pt = [&](int k, uint64_t d) { dig[hf][k] = d; };
+                tcd::mul_rows_f<ND, false, decltype(ag), decltype(bg), decltype(lo), decltype(li), decltype(pt), NR>(
+                    ag, bg, lo, li, pt);
+            }
+            uint64_t sum[2 * ND + 1] = {0}, c = 0;
+            for (int k = 0; k < 2 * ND; k++) {
+                uint64_t v = c;
+                if (k < ND + NR) v += dig[0][k];
+                if (k >= NR && k - NR < ND + NR) v += dig[1][k - NR];
+                sum[k] = v & f64::M52;
+                c = v >> 52;
+            }
+            for (int k = 0; k < 2 * ND; k++) put(k, sum[k]);
         } else if (op == "W") {
             for (int k = 0; k < ND; k++) put(k, (uint64_t)a[k]);
             for (int k = ND; k < 2 * ND; k++) put(k, 0);
