@@ -23,8 +23,7 @@ tc_redc_test(const uint32_t* __restrict__ T, uint32_t* __restrict__ U, uint32_t*
     const int warp = threadIdx.x / 32;
     if (warp == 0) tmem_alloc(smem_u32(&sh.tmem_base), 512);
     if (threadIdx.x == 0) {
-        mbar_init(smem_u32(&sh.mbar[0]), 1);
-        mbar_init(smem_u32(&sh.mbar[1]), 1);
+        for (int i = 0; i < 2; i++) mbar_init(smem_u32(&sh.mbar[i]), 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     build_strips(sh, npb, nb);

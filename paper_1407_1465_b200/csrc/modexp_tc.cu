@@ -110,7 +110,7 @@ __global__ void __launch_bounds__(TcCfg<S>::BLOCK, 1) modexp_tc_kernel(const __g
     const int warp = threadIdx.x / 32;
     if (warp == 0) tc::tmem_alloc(tc::smem_u32(&sh.tmem_base), C::TMEM_COLS);
     if (threadIdx.x == 0) {
-        for (int i = 0; i < C::TILES; i++) tc::mbar_init(tc::smem_u32(&sh.mbar[i]), 1);
+        for (int i = 0; i < (int)(sizeof(sh.mbar) / sizeof(sh.mbar[0])); i++) tc::mbar_init(tc::smem_u32(&sh.mbar[i]), 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     tc::build_strips(sh, p.npb, reinterpret_cast<const uint8_t*>(ip.n));

@@ -64,7 +64,9 @@ struct __align__(16) TcShared {
     uint8_t np_strip[G::NP_STRIP_BYTES];
     uint8_t n_strip[G::N_STRIP_BYTES];
     uint32_t nw[G::NW];                       // n as words (conditional subtraction)
-    unsigned long long mbar[TILES];
+    // per tile; at KB = 512 a second one per tile (index TILES + tile, the address
+    // mbar + 8 TILES): GEMM2's first N half (RSA_TC_SPLIT512)
+    unsigned long long mbar[KB == 512 ? 2 * TILES : TILES];
     uint32_t tmem_base;
 };
 
@@ -107,6 +109,24 @@ __device__ __forceinline__ void issue_gemm1(TcShared<KB, TILES>& sh, int tile, u
             const uint64_t b = sdesc(sp + (c0 - 32 * I - G::NP_RHO0) * 16, G::NP_LBO, 128);
             mma_u8(tmem + c0, a, b, id, I > 0);
         }
+    }
+}
+
+#ifndef RSA_TC_SPLIT512
+#define RSA_TC_SPLIT512 1   // KB = 512: GEMM2's two N halves completed separately (the first half's
+#endif                      // carries resolve while the second computes; its readout writes registers only)
+
+// one N block (h) of GEMM2
+template <int KB, int TILES>
+__device__ __forceinline__ void issue_gemm2_half(TcShared<KB, TILES>& sh, int tile, uint32_t tmem, int h) {
+    using G = Geom<KB>;
+    const uint32_t st = smem_u32(sh.stage[tile]), sn = smem_u32(sh.n_strip);
+    constexpr uint32_t id = idesc_u8(128, G::G2_N);
+#pragma unroll
+    for (int I = 0; I < KB / 32; I++) {
+        const uint64_t a = sdesc(st + 2 * I * STAGE_LBO, STAGE_LBO, 128);
+        const uint64_t b = sdesc(sn + (G::G2_C0 + G::G2_N * h - 32 * I - G::N_RHO0) * 16, G::N_LBO, 128);
+        mma_u8(tmem + G::G2_N * h, a, b, id, I > 0);
     }
 }
 
@@ -169,7 +189,7 @@ struct TcTile {
     uint32_t tmem;     // this tile's first TMEM column (lane 0)
     uint32_t tlane;    // this warp's lane offset (32 (warp % 4)) << 16
     uint32_t mbar;
-    uint32_t phase;
+    uint32_t phase;    // bit 0: mbar's parity; bit 1 (KB = 512 split): the second barrier's
 };
 
 // U = (T + m n) / R reduced below n.  On entry T_low (words 0..63) is in the
@@ -192,7 +212,7 @@ __device__ __forceinline__ void redc(TcShared<KB, TILES>& sh, TcTile& tt, uint32
         issue_gemm1(sh, tile, tt.tmem);
         commit(tt.mbar);
     }
-    mbar_wait(tt.mbar, tt.phase);
+    mbar_wait(tt.mbar, tt.phase & 1);
     tt.phase ^= 1;
     fence_after();
     uint32_t hprev = 0;
@@ -225,9 +245,16 @@ __device__ __forceinline__ void redc(TcShared<KB, TILES>& sh, TcTile& tt, uint32
     fence_async_smem();
     fence_before();
     bar_sync(1 + tile, TILE);
+    constexpr bool SPLIT2 = (Geom<KB>::G2_NB == 2) && RSA_TC_SPLIT512;
     if (r == 0) {
         fence_after();
-        issue_gemm2(sh, tile, tt.tmem);
+        if constexpr (SPLIT2) {
+            issue_gemm2_half(sh, tile, tt.tmem, 0);
+            commit(tt.mbar + 8 * TILES);
+            issue_gemm2_half(sh, tile, tt.tmem, 1);
+        } else {
+            issue_gemm2(sh, tile, tt.tmem);
+        }
         commit(tt.mbar);
     }
     // columns 2KB-4 .. 2KB-2 (the top byte products) meanwhile
@@ -236,8 +263,13 @@ __device__ __forceinline__ void redc(TcShared<KB, TILES>& sh, TcTile& tt, uint32
     const uint32_t c508 = m253 * n255 + m254 * n254 + m255 * n253;
     const uint32_t c509 = m254 * n255 + m255 * n254;
     const uint32_t c510 = m255 * n255;
-    mbar_wait(tt.mbar, tt.phase);
-    tt.phase ^= 1;
+    if constexpr (SPLIT2) {
+        mbar_wait(tt.mbar + 8 * TILES, (tt.phase >> 1) & 1);
+        tt.phase ^= 2;
+    } else {
+        mbar_wait(tt.mbar, tt.phase & 1);
+        tt.phase ^= 1;
+    }
     fence_after();
     // TMEM column idx = global column KB-4 + idx.  Word w of U (bits 8 KB + 32 w)
     // is P_w over global columns KB + 4w .. KB + 3 + 4w = idx 4 + 4w .. 7 + 4w.
@@ -245,6 +277,11 @@ __device__ __forceinline__ void redc(TcShared<KB, TILES>& sh, TcTile& tt, uint32
     uint32_t carry = 0;
 #pragma unroll
     for (int ch = 0; ch < NCH; ch++) {
+        if (SPLIT2 && ch == NCH / 2) {     // second N half complete
+            mbar_wait(tt.mbar, tt.phase & 1);
+            tt.phase ^= 1;
+            fence_after();
+        }
         uint32_t v[32];
         tmem_ld32(tt.tmem + tt.tlane + 32 * ch, v);
         tmem_ld_wait();
