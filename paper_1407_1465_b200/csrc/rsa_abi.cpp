@@ -628,18 +628,29 @@ int rsa_modexp_batch_host(const uint32_t* base_host, const uint32_t* exp, const 
     if (nch < 1) nch = 1;
     const size_t per = ((waves + nch - 1) / nch) * wave;
     nch = (count + per - 1) / per;
-    cudaStream_t ss[2];
-    if (cudaStreamCreateWithFlags(&ss[0], cudaStreamNonBlocking) != cudaSuccess) return RSA_ECUDA;
-    if (cudaStreamCreateWithFlags(&ss[1], cudaStreamNonBlocking) != cudaSuccess) {
-        cudaStreamDestroy(ss[0]);
-        return RSA_ECUDA;
-    }
+    // two non-blocking streams per (host thread, device), created once: creating and
+    // destroying them per call dominated small calls (the paper's 9-packet workload)
+    struct StreamPair {
+        cudaStream_t s[64][2] = {};
+        ~StreamPair() {
+            for (auto& d : s)
+                for (auto& x : d)
+                    if (x) cudaStreamDestroy(x);
+        }
+    };
+    thread_local StreamPair tl_streams;
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return RSA_ECUDA;
+    cudaStream_t* ss = tl_streams.s[dev];
+    for (int k = 0; k < 2; k++)
+        if (!ss[k] && cudaStreamCreateWithFlags(&ss[k], cudaStreamNonBlocking) != cudaSuccess) return RSA_ECUDA;
     keep_pool_memory();
+    const int nstreams = nch > 1 ? 2 : 1;
     uint32_t* dbuf[2] = {nullptr, nullptr};
     void* tab[2] = {nullptr, nullptr};
     const size_t tb = table_bytes(pl);
     int rc = RSA_OK;
-    for (int k = 0; k < 2 && rc == RSA_OK; k++) {
+    for (int k = 0; k < nstreams && rc == RSA_OK; k++) {
         if (cudaMallocAsync((void**)&dbuf[k], per * row, ss[k]) != cudaSuccess) rc = RSA_ECUDA;
         if (tb && rc == RSA_OK && cudaMallocAsync(&tab[k], tb, ss[k]) != cudaSuccess) rc = RSA_ECUDA;
     }
@@ -658,11 +669,10 @@ int rsa_modexp_batch_host(const uint32_t* base_host, const uint32_t* exp, const 
         if (cudaMemcpyAsync(out_host + lo * s, d, cnt * row, cudaMemcpyDeviceToHost, sc) != cudaSuccess)
             rc = RSA_ECUDA;
     }
-    for (int k = 0; k < 2; k++) {
+    for (int k = 0; k < nstreams; k++) {
         if (dbuf[k]) cudaFreeAsync(dbuf[k], ss[k]);
         if (tab[k]) cudaFreeAsync(tab[k], ss[k]);
         if (cudaStreamSynchronize(ss[k]) != cudaSuccess) rc = RSA_ECUDA;
-        cudaStreamDestroy(ss[k]);
     }
     return rc;
 }
