@@ -1,6 +1,6 @@
 // mont_tc.cuh -- Montgomery reduction of a 128-packet tile on the tensor core
 // (operands of KB bytes, R = 2^(8 KB), n < R odd, byte digits for the MMAs;
-// KB = 256 for the 2048-bit class, 128 for the 1024-bit class.  The numbers
+// KB = 128 / 256 / 512 for the 1024- / 2048- / 4096-bit classes.  The numbers
 // below are for KB = 256; every column index scales with KB).
 //
 // The operation is the reduction half of Fig 3's "(u*v) mod m" (PAPER.md:89,
@@ -14,15 +14,16 @@
 // Both products have a constant operand (n', n: one key per batch), so for a
 // tile of 128 packets they are [128 x 256] x [256 x N] u8 matrix products on
 // the tensor core (tc_i8.cuh) against Toeplitz matrices, read out of TMEM as
-// exact column sums c_j = sum_k x_k y_{j-k} (< 2^24) whose carries the
-// thread of each packet resolves:
+// exact column sums c_j = sum_k x_k y_{j-k} (<= KB 255^2: < 2^24 at KB <= 256,
+// < 2^25 at 512; s32 accumulators) whose carries the thread of each packet
+// resolves:
 //   GEMM1: columns 0..255 of T_low x n'   (two N = 128 blocks; the upper
 //          block-triangle is zero and skipped: 12 MMAs of K = 32)
 //   GEMM2: columns 252..507 of m x n       (8 MMAs, N = 256); columns
 //          508..510 (6 byte products) on the CUDA cores.
 // The carry out of the low half of T + m n: its value V = (T_low + sum_{j<256}
 // c_j 2^(8j)) / R is an integer (T + m n = 0 mod R), and columns below 252
-// move V 2^32 by less than 2^17 (c_j < 2^24), so V = ceil(X / 2^32) with
+// move V 2^32 by less than 2^18 (c_j < 2^25), so V = ceil(X / 2^32) with
 // X = T_low's top word + c_252 + c_253 2^8 + c_254 2^16 + c_255 2^24.
 //
 // Shared memory (per CTA of two tiles): the n' and n "strips" (every
