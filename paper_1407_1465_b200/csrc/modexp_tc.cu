@@ -293,8 +293,7 @@ __global__ void __launch_bounds__(TcCfg<S>::BLOCK, 1) modexp_tc_kernel(const __g
                         if (op.kind == RSA_OP_R2) return r2d[j];
                         return j == 0 ? 1.0 : 0.0;                   // RSA_OP_ONE (no MULX at S = 128)
                     };
-                    uint64_t eacc = 0;
-                    int enb = 0, ew = 0;
+                    int ew = 0;
                     auto emit = [&](uint32_t v) {
                         if (ew < NW) {
                             reinterpret_cast<uint32_t*>(sh.stage[tt.tile] + (ew >> 2) * tc::STAGE_LBO +
@@ -307,21 +306,8 @@ __global__ void __launch_bounds__(TcCfg<S>::BLOCK, 1) modexp_tc_kernel(const __g
                         }
                         ew++;
                     };
-                    // digit d (52 bits) joins the enb < 32 pending bits; whole words leave
-                    auto lout = [&](int, uint64_t d) {
-                        const uint64_t lo64 = eacc | (d << enb);
-                        const uint64_t hi = enb > 12 ? (d >> (64 - enb)) : 0;
-                        emit((uint32_t)lo64);
-                        uint64_t rest = (lo64 >> 32) | (hi << 32);
-                        int nb = enb + 20;
-                        if (nb >= 32) {
-                            emit((uint32_t)rest);
-                            rest >>= 32;
-                            nb -= 32;
-                        }
-                        eacc = rest;
-                        enb = nb;
-                    };
+                    tcd::WordEmitter<decltype(emit)> we{emit, 0, 0};
+                    auto lout = [&](int, uint64_t d) { we.digit(d); };
                     auto lin = [&](int) -> uint64_t { return 0; };
                     tcd::mul_rows_f<ND, false>(get_digit_rows, bget, lout, lin, put);
                 } else {

@@ -98,6 +98,30 @@ __host__ __device__ __forceinline__ void mul_rows(const double (&a)[ND], BF b, L
     mul_rows_f<ND, true>([&](int i) -> double { return a[i]; }, b, lowout, lowin, put);
 }
 
+// digit stream -> 32-bit words at RUN TIME (digits arrive inside a rolled loop):
+// each 52-bit digit joins the < 32 pending bits in a 64-bit buffer and whole
+// words leave through emit(v), in order (one or two per digit).
+template <typename Emit>
+struct WordEmitter {
+    Emit emit;
+    uint64_t acc;
+    int nb;
+    __host__ __device__ __forceinline__ void digit(uint64_t d) {
+        const uint64_t lo64 = acc | (d << nb);
+        const uint64_t hi = nb > 12 ? (d >> (64 - nb)) : 0;   // bits 64 .. nb + 51
+        emit((uint32_t)lo64);
+        uint64_t rest = (lo64 >> 32) | (hi << 32);
+        int n = nb + 20;
+        if (n >= 32) {
+            emit((uint32_t)rest);
+            rest >>= 32;
+            n -= 32;
+        }
+        acc = rest;
+        nb = n;
+    }
+};
+
 // digit stream -> 32-bit words (words 0 .. NWORDS-1; bits beyond are dropped).
 // put(k, d) must be called for k = 0, 1, 2, ... in order.
 template <int NWORDS, typename Word>

@@ -81,3 +81,10 @@ def test_words_digits_roundtrip(model):
     rng = random.Random(10)
     for a, _ in operands(rng):
         assert model(f"W {a:x}") == a
+
+
+def test_runtime_word_emitter(model):
+    """The 4096-bit kernel's run-time packer (digits leave a rolled loop as words)."""
+    rng = random.Random(13)
+    for a, _ in operands(rng):
+        assert model(f"E {a:x}") == a

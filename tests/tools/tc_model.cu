@@ -8,6 +8,7 @@
 //   R a     T = A^2 through sqr_col (compile-time-expanded scan, batch 2: the 2048-bit TC kernel)
 //   H a     the 1024-bit class (ND = 20, a < 2^1024): T = A^2 through sqr_col (batch 4), 64 words
 //   W x     x (64 words) -> 40 digits (words_to_digits) -> back to words (Packer)
+//   E x     x (64 words) -> 40 digits -> words again through the run-time WordEmitter
 //   P a b   A B as two row halves (mul_rows_f with NR = 20 on b_0..19 and b_20..39), summed
 #include <cfenv>
 #include <cstdint>
@@ -96,6 +97,11 @@ int main() {
                 c = v >> 52;
             }
             for (int k = 0; k < 2 * ND; k++) put(k, sum[k]);
+        } else if (op == "E") {
+            int ew = 0;
+            auto emit = [&](uint32_t v) { if (ew < 2 * NW) out[ew] = v; ew++; };
+            tcd::WordEmitter<decltype(emit)> we{emit, 0, 0};
+            for (int k = 0; k < ND; k++) we.digit((uint64_t)a[k]);
         } else if (op == "W") {
             for (int k = 0; k < ND; k++) put(k, (uint64_t)a[k]);
             for (int k = ND; k < 2 * ND; k++) put(k, 0);
