@@ -88,18 +88,22 @@ int rsa_validate_key(const uint32_t* e, const uint32_t* d, const uint32_t* p,
  *               workspace allocation) and returns; completion is observed
  *               through the stream.  count == 0 is a no-op returning RSA_OK.
  * Kernels (results identical; chosen by measurement): moduli of
- * 513..4096 bits run on the FP64 pipe (52-bit digits, exact DFMA.RZ products),
- * narrower ones on the integer (IMAD) pipe; rsa_set_kernel_path (below)
- * selects the alternates per width class for A/B measurement.
+ * 513..4096 bits run the tensor-core path (the product A B on the FP64 pipe,
+ * 52-bit digits with exact DFMA.RZ products; the Montgomery reduction by the
+ * batch's modulus as u8 tcgen05 matrix products), narrower ones the integer
+ * (IMAD) pipe; rsa_set_kernel_path (below) selects the alternates per width
+ * class for A/B measurement.  The tensor-core kernels hold all 512 TMEM
+ * columns of their SM while resident.
  * Errors: RSA_EINVAL, RSA_ERANGE, RSA_EEVEN, RSA_ECUDA. */
 int rsa_modexp_batch(const uint32_t* base, const uint32_t* exp, const uint32_t* n,
                      int nbits, size_t count, uint32_t* out, void* stream);
 
 /* Same operation end to end from HOST memory: copies base_host to the device,
  * exponentiates, and copies the result back to out_host, pipelining chunks
- * so copies overlap compute (two streams).  base_host/out_host may be
- * pageable or pinned (pinned is faster).  Synchronous: returns when out_host
- * is written.  Errors: as rsa_modexp_batch. */
+ * so copies overlap compute (two streams, created once per calling host
+ * thread and device and reused; one stream for a single-chunk call).
+ * base_host/out_host may be pageable or pinned (pinned is faster).
+ * Synchronous: returns when out_host is written.  Errors: as rsa_modexp_batch. */
 int rsa_modexp_batch_host(const uint32_t* base_host, const uint32_t* exp, const uint32_t* n,
                           int nbits, size_t count, uint32_t* out_host);
 
