@@ -68,6 +68,10 @@ namespace rsa_b200 {
 #define RSA_TC_SQROWS128 1  // 4096-bit squarings by the rolled row form: ND^2 = 6400 digit products instead
 #endif                      // of 3240, but a few KB of code: A/B 70.4K vs 57.8K decrypts/s (the ~300 KB
                             // expanded scan starves on instruction fetch at 4 warps/SM: no_instruction 2.2)
+#ifndef RSA_TC_BSPEC128
+#define RSA_TC_BSPEC128 1   // 4096-bit row loop instantiated per B source: A/B 75.2K vs 71.3K (the per-row
+                            // run-time dispatch on the op kind sat in the loop)
+#endif
 #ifndef RSA_TC_APAIR
 #define RSA_TC_APAIR 0      // 4096-bit A slot as digit pairs (A/B)
 #endif
@@ -309,7 +313,22 @@ __global__ void __launch_bounds__(TcCfg<S>::BLOCK, 1) modexp_tc_kernel(const __g
                     tcd::WordEmitter<decltype(emit)> we{emit, 0, 0};
                     auto lout = [&](int, uint64_t d) { we.digit(d); };
                     auto lin = [&](int) -> uint64_t { return 0; };
-                    tcd::mul_rows_f<ND, false>(get_digit_rows, bget, lout, lin, put);
+                    if constexpr (RSA_TC_BSPEC128 != 0) {
+                        // one row-loop instance per B source: the per-row fetch is a single load
+                        if (op.kind == RSA_OP_SQR) {
+                            tcd::mul_rows_f<ND, false>(get_digit_rows, get_digit, lout, lin, put);
+                        } else if (op.kind == RSA_OP_MUL) {
+                            auto btab = [&](int j) -> double {
+                                const double2 v = table[((size_t)op.bidx * NP + (j >> 1)) * nthr + gtid];
+                                return (j & 1) ? v.y : v.x;
+                            };
+                            tcd::mul_rows_f<ND, false>(get_digit_rows, btab, lout, lin, put);
+                        } else {
+                            tcd::mul_rows_f<ND, false>(get_digit_rows, bget, lout, lin, put);
+                        }
+                    } else {
+                        tcd::mul_rows_f<ND, false>(get_digit_rows, bget, lout, lin, put);
+                    }
                 } else {
                     // rows, rolled (the unrolled column scan is ~160 KB of code);
                     // T's low digits go back into b's slot as b's digits are used up
