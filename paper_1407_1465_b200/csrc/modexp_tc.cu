@@ -72,6 +72,9 @@ namespace rsa_b200 {
 #define RSA_TC_BSPEC128 1   // 4096-bit row loop instantiated per B source: A/B 75.2K vs 71.3K (the per-row
                             // run-time dispatch on the op kind sat in the loop)
 #endif
+#ifndef RSA_TC_EMITSEL
+#define RSA_TC_EMITSEL 2    // 4096-bit run-time word stores: 0 branches, 1 branch-free stores, 2 + branch-free second word
+#endif
 #ifndef RSA_TC_APAIR
 #define RSA_TC_APAIR 0      // 4096-bit A slot as digit pairs (A/B)
 #endif
@@ -110,6 +113,7 @@ __global__ void __launch_bounds__(TcCfg<S>::BLOCK, 1) modexp_tc_kernel(const __g
     Shared& sh = *reinterpret_cast<Shared*>(smem_raw);
     double* const bslot = reinterpret_cast<double*>(smem_raw + sizeof(Shared)) + threadIdx.x;
     __shared__ __align__(16) double r2d[ND];
+    __shared__ uint32_t tc_ovf[C::SLOTA && RSA_TC_EMITSEL ? 3 * TC_BLOCK : 1];   // S = 128: T words NW, NW+1, scratch
     const ModexpParams<TC_S>& ip = p.f.ip;
     const int warp = threadIdx.x / 32;
     if (warp == 0) tc::tmem_alloc(tc::smem_u32(&sh.tmem_base), C::TMEM_COLS);
@@ -298,8 +302,20 @@ __global__ void __launch_bounds__(TcCfg<S>::BLOCK, 1) modexp_tc_kernel(const __g
                         return j == 0 ? 1.0 : 0.0;                   // RSA_OP_ONE (no MULX at S = 128)
                     };
                     int ew = 0;
+                    // branch-free (RSA_TC_EMITSEL): words >= NW (digit ND-1's top bits) go to a small
+                    // overflow area, and a digit's second word, when it has none, to a scratch slot
+                    auto emit_sel = [&](uint32_t v, bool valid) {
+                        uint32_t* const sp = reinterpret_cast<uint32_t*>(sh.stage[tt.tile] + (ew >> 2) * tc::STAGE_LBO +
+                                                                         tt.r * 16) + (ew & 3);
+                        uint32_t* const op_ = tc_ovf + (ew - NW) * TC_BLOCK + threadIdx.x;
+                        uint32_t* const dst = ew < NW ? sp : op_;
+                        *(valid ? dst : tc_ovf + 2 * TC_BLOCK + threadIdx.x) = v;
+                        ew += valid ? 1 : 0;
+                    };
                     auto emit = [&](uint32_t v) {
-                        if (ew < NW) {
+                        if constexpr (RSA_TC_EMITSEL == 1) {
+                            emit_sel(v, true);
+                        } else if (ew < NW) {
                             reinterpret_cast<uint32_t*>(sh.stage[tt.tile] + (ew >> 2) * tc::STAGE_LBO +
                                                         tt.r * 16)[ew & 3] = v;
                             if (ew == NW - 1) t63 = v;
@@ -311,7 +327,11 @@ __global__ void __launch_bounds__(TcCfg<S>::BLOCK, 1) modexp_tc_kernel(const __g
                         ew++;
                     };
                     tcd::WordEmitter<decltype(emit)> we{emit, 0, 0};
-                    auto lout = [&](int, uint64_t d) { we.digit(d); };
+                    tcd::WordEmitter<decltype(emit_sel), true> wes{emit_sel, 0, 0};
+                    auto lout = [&](int, uint64_t d) {
+                        if constexpr (RSA_TC_EMITSEL == 2) wes.digit(d);
+                        else we.digit(d);
+                    };
                     auto lin = [&](int) -> uint64_t { return 0; };
                     if constexpr (RSA_TC_BSPEC128 != 0) {
                         // one row-loop instance per B source: the per-row fetch is a single load
@@ -328,6 +348,12 @@ __global__ void __launch_bounds__(TcCfg<S>::BLOCK, 1) modexp_tc_kernel(const __g
                         }
                     } else {
                         tcd::mul_rows_f<ND, false>(get_digit_rows, bget, lout, lin, put);
+                    }
+                    if constexpr (RSA_TC_EMITSEL != 0) {
+                        t63 = reinterpret_cast<const uint32_t*>(sh.stage[tt.tile] + ((NW - 1) >> 2) * tc::STAGE_LBO +
+                                                                tt.r * 16)[(NW - 1) & 3];
+                        th[0] = tc_ovf[threadIdx.x];
+                        th[1] = tc_ovf[TC_BLOCK + threadIdx.x];
                     }
                 } else {
                     // rows, rolled (the unrolled column scan is ~160 KB of code);

@@ -101,7 +101,10 @@ __host__ __device__ __forceinline__ void mul_rows(const double (&a)[ND], BF b, L
 // digit stream -> 32-bit words at RUN TIME (digits arrive inside a rolled loop):
 // each 52-bit digit joins the < 32 pending bits in a 64-bit buffer and whole
 // words leave through emit(v), in order (one or two per digit).
-template <typename Emit>
+// SEL: no branches; emit(v, valid) is called twice per digit, the second time
+// with valid = whether the digit completed a second word (the emitter stores
+// an invalid word to a scratch slot and does not advance).
+template <typename Emit, bool SEL = false>
 struct WordEmitter {
     Emit emit;
     uint64_t acc;
@@ -109,13 +112,21 @@ struct WordEmitter {
     __host__ __device__ __forceinline__ void digit(uint64_t d) {
         const uint64_t lo64 = acc | (d << nb);
         const uint64_t hi = nb > 12 ? (d >> (64 - nb)) : 0;   // bits 64 .. nb + 51
-        emit((uint32_t)lo64);
         uint64_t rest = (lo64 >> 32) | (hi << 32);
         int n = nb + 20;
-        if (n >= 32) {
-            emit((uint32_t)rest);
-            rest >>= 32;
-            n -= 32;
+        if constexpr (SEL) {
+            emit((uint32_t)lo64, true);
+            const bool two = n >= 32;
+            emit((uint32_t)rest, two);
+            rest = two ? rest >> 32 : rest;
+            n = two ? n - 32 : n;
+        } else {
+            emit((uint32_t)lo64);
+            if (n >= 32) {
+                emit((uint32_t)rest);
+                rest >>= 32;
+                n -= 32;
+            }
         }
         acc = rest;
         nb = n;

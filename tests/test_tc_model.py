@@ -83,8 +83,10 @@ def test_words_digits_roundtrip(model):
         assert model(f"W {a:x}") == a
 
 
-def test_runtime_word_emitter(model):
-    """The 4096-bit kernel's run-time packer (digits leave a rolled loop as words)."""
+@pytest.mark.parametrize("op", ["E", "F"])
+def test_runtime_word_emitter(model, op):
+    """The 4096-bit kernel's run-time packer (digits leave a rolled loop as
+    words), with branches (E) and branch-free (F, the kernel's default)."""
     rng = random.Random(13)
     for a, _ in operands(rng):
-        assert model(f"E {a:x}") == a
+        assert model(f"{op} {a:x}") == a

@@ -97,11 +97,16 @@ int main() {
                 c = v >> 52;
             }
             for (int k = 0; k < 2 * ND; k++) put(k, sum[k]);
-        } else if (op == "E") {
+        } else if (op == "E" || op == "F") {
             int ew = 0;
             auto emit = [&](uint32_t v) { if (ew < 2 * NW) out[ew] = v; ew++; };
+            auto emit_sel = [&](uint32_t v, bool valid) { if (valid && ew < 2 * NW) out[ew] = v; ew += valid; };
             tcd::WordEmitter<decltype(emit)> we{emit, 0, 0};
-            for (int k = 0; k < ND; k++) we.digit((uint64_t)a[k]);
+            tcd::WordEmitter<decltype(emit_sel), true> wes{emit_sel, 0, 0};
+            for (int k = 0; k < ND; k++) {
+                if (op == "E") we.digit((uint64_t)a[k]);
+                else wes.digit((uint64_t)a[k]);
+            }
         } else if (op == "W") {
             for (int k = 0; k < ND; k++) put(k, (uint64_t)a[k]);
             for (int k = ND; k < 2 * ND; k++) put(k, 0);
