@@ -86,6 +86,8 @@ def parse():
     ap.add_argument("--kernel-path", action="append", default=[], metavar="S=PATH",
                     help="A/B only: run width class S on another kernel (rsa_set_kernel_path), PATH one of "
                          "tc, fp64, int, int_group, int_pair, int_multi; e.g. --kernel-path 64=fp64")
+    ap.add_argument("--window", type=int, default=0,
+                    help="A/B only: force the sliding-window width (rsa_set_window; 0 = the plan's cost model)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=20.0, help="CPU-seconds budget of the oracle sample")
@@ -362,6 +364,8 @@ def run_ours(args, rank, world, local_rank):
     for kp in args.kernel_path:
         cls, path = kp.split("=")
         R.rsa_set_kernel_path(int(cls), getattr(R, "RSA_PATH_" + path.upper()))
+    if args.window:
+        R.rsa_set_window(args.window)
     key_name, total, legs = WORKLOADS[args.config]
     if args.count:
         total = args.count
@@ -685,6 +689,7 @@ def run_ours(args, rank, world, local_rank):
             "vs_baseline": None, "dtype": "f64+u8" if tc else ("f64" if fp64 else "u32"), "data": "synthetic",
             "config": {"workload": args.config, "packets_total": total, "packets_per_rank": per,
                        **({"kernel_path": args.kernel_path} if args.kernel_path else {}),
+                       **({"window_forced": args.window} if args.window else {}),
                        "key": key_name + " (seeded, "
                        "workload/keys.json)", "legs": [l for l, _ in legs], "modulus_bits": nb,
                        "l2": f"inputs {count * s * 4 / 2**20:.0f} MiB per leg vs 126 MB L2"
