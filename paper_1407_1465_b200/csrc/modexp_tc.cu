@@ -75,6 +75,9 @@ namespace rsa_b200 {
 #ifndef RSA_TC_EMITSEL
 #define RSA_TC_EMITSEL 2    // 4096-bit run-time word stores: 0 branches, 1 branch-free stores, 2 + branch-free second word
 #endif
+#ifndef RSA_TC_SQBLK128
+#define RSA_TC_SQBLK128 10  // 4096-bit squarings by the rolled block triangle (tcd::sqr_blocks, blocks of this
+#endif                      // many digits; 3240 digit products instead of the row form's 6400; 0 = rows)
 #ifndef RSA_TC_APAIR
 #define RSA_TC_APAIR 0      // 4096-bit A slot as digit pairs (A/B)
 #endif
@@ -336,7 +339,14 @@ __global__ void __launch_bounds__(TcCfg<S>::BLOCK, 1) modexp_tc_kernel(const __g
                     if constexpr (RSA_TC_BSPEC128 != 0) {
                         // one row-loop instance per B source: the per-row fetch is a single load
                         if (op.kind == RSA_OP_SQR) {
-                            tcd::mul_rows_f<ND, false>(get_digit_rows, get_digit, lout, lin, put);
+                            if constexpr (RSA_TC_SQBLK128 != 0) {
+                                // T's high digits go over A's dead blocks, then to th through put
+                                auto hiout = [&](int k, uint64_t d) { *slot_at(k) = f64::from_bits(d); };
+                                auto hiin = [&](int k) -> uint64_t { return f64::bits(get_digit(k)); };
+                                tcd::sqr_blocks<ND, RSA_TC_SQBLK128>(get_digit, lout, hiout, hiin, put);
+                            } else {
+                                tcd::mul_rows_f<ND, false>(get_digit_rows, get_digit, lout, lin, put);
+                            }
                         } else if (op.kind == RSA_OP_MUL) {
                             auto btab = [&](int j) -> double {
                                 const double2 v = table[((size_t)op.bidx * NP + (j >> 1)) * nthr + gtid];
@@ -427,7 +437,7 @@ static cudaError_t launch_tc(const void* params, int sms, cudaStream_t stream, i
 
 // 1 if class S's squarings run a dedicated squaring (ND (ND+1)/2 digit products on
 // the CUDA cores), 0 if the row-form product (ND^2)
-int rsa_b200_tc_sqr(int S) { return (S == 128 && RSA_TC_SQROWS128) ? 0 : 1; }
+int rsa_b200_tc_sqr(int S) { return (S == 128 && RSA_TC_SQROWS128 && !(RSA_TC_BSPEC128 && RSA_TC_SQBLK128)) ? 0 : 1; }
 
 cudaError_t rsa_b200_launch_tc(int S, const void* params, int sms, cudaStream_t stream, int* grid, int* block,
                                size_t* slots, bool query_only) {

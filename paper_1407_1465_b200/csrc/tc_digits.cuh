@@ -98,6 +98,102 @@ __host__ __device__ __forceinline__ void mul_rows(const double (&a)[ND], BF b, L
     mul_rows_f<ND, true>([&](int i) -> double { return a[i]; }, b, lowout, lowin, put);
 }
 
+// sqr_blocks: T = A^2 with the triangle's ND (ND+1) / 2 digit products in a
+// ROLLED loop (mul_rows_f's A A costs ND^2; the unrolled column scan sqr_col
+// is too much code at ND = 80).  A's digits are cut into NB = ND / BS blocks;
+// step s (0 .. 2 NB - 1) adds every block pair (p, s - p), p < s - p, as a
+// static BS x BS product, and for even s the diagonal block's strict upper
+// triangle, into a 2 BS-column window w (column BS s + d), then finishes
+// columns BS s .. BS s + BS - 1:
+//   T_c = 2 (W_c - bias_c) + [a_{c/2}^2's low (c even) / high (c odd) half] + carry,
+// bias_c = nl(c) BL + nl(c - 1) BH with nl(c) = #{i < j < ND : i + j = c} (the
+// exponent fields of the summed bit patterns), and slides the window by BS.
+// Columns 0 .. ND-1 leave through lowout(c, digit); columns ND + k through
+// hiout(k, digit) -- the caller may store them over A's block s - NB, which no
+// later step reads -- and are replayed from hiin(k) into put(ND + k) at the end.
+template <int ND, int BS, typename AF, typename LO, typename HO, typename HI, typename Put>
+__host__ __device__ __forceinline__ void sqr_blocks(AF a, LO lowout, HO hiout, HI hiin, Put put) {
+    static_assert(ND % BS == 0 && BS % 2 == 0, "blocks");
+    constexpr int NB = ND / BS;
+    uint64_t w[2 * BS];
+#pragma unroll
+    for (int d = 0; d < 2 * BS; d++) w[d] = 0;
+    uint64_t carry = 0;
+    auto nl = [](int c) -> uint64_t {          // pairs i < j < ND with i + j = c
+        const int lo = c - ND + 1 > 0 ? c - ND + 1 : 0, hi = (c + 1) / 2;
+        return hi > lo ? (uint64_t)(hi - lo) : 0;
+    };
+#ifdef __CUDA_ARCH__
+#pragma unroll 1
+#endif
+    for (int s = 0; s < 2 * NB; s++) {
+        const int pmin = s - (NB - 1) > 0 ? s - (NB - 1) : 0, pend = (s + 1) / 2;   // p < s - p
+#ifdef __CUDA_ARCH__
+#pragma unroll 1
+#endif
+        for (int p = pmin; p < pend; p++) {
+            double x[BS], y[BS];
+#pragma unroll
+            for (int k = 0; k < BS; k++) {
+                x[k] = a(BS * p + k);
+                y[k] = a(BS * (s - p) + k);
+            }
+#pragma unroll
+            for (int i = 0; i < BS; i++) {
+                uint64_t hp = 0;
+#pragma unroll
+                for (int k = 0; k < BS; k++) {
+                    const double h = fma_rz(x[k], y[i], C104);
+                    const double l = fma_rz(x[k], y[i], sub_rn(C2, h));
+                    w[i + k] += bits(l) + hp;
+                    hp = bits(h);
+                }
+                w[i + BS] += hp;
+            }
+        }
+        if ((s & 1) == 0 && s / 2 < NB) {      // diagonal block s / 2: pairs k1 < k2
+            double x[BS];
+#pragma unroll
+            for (int k = 0; k < BS; k++) x[k] = a(BS * (s / 2) + k);
+#pragma unroll
+            for (int k1 = 0; k1 < BS - 1; k1++) {
+                uint64_t hp = 0;
+#pragma unroll
+                for (int k2 = k1 + 1; k2 < BS; k2++) {
+                    const double h = fma_rz(x[k1], x[k2], C104);
+                    const double l = fma_rz(x[k1], x[k2], sub_rn(C2, h));
+                    w[k1 + k2] += bits(l) + hp;
+                    hp = bits(h);
+                }
+                w[k1 + BS] += hp;
+            }
+        }
+        // finish columns BS s + d: the digit squares a_i^2, i = BS s / 2 + m
+#pragma unroll
+        for (int m = 0; m < BS / 2; m++) {
+            const double ai = a(BS * s / 2 + m);
+            const double h = fma_rz(ai, ai, C104);
+            const double l = fma_rz(ai, ai, sub_rn(C2, h));
+#pragma unroll
+            for (int e = 0; e < 2; e++) {
+                const int d = 2 * m + e, c = BS * s + d;
+                const uint64_t bias = nl(c) * BL + nl(c - 1) * BH;
+                const uint64_t v = 2 * (w[d] - bias) + (e ? bits(h) - BH : bits(l) - BL) + carry;
+                carry = v >> D;
+                if (c < ND) lowout(c, v & M52);
+                else hiout(c - ND, v & M52);
+            }
+        }
+#pragma unroll
+        for (int d = 0; d < BS; d++) {
+            w[d] = w[d + BS];
+            w[d + BS] = 0;
+        }
+    }
+#pragma unroll
+    for (int k = 0; k < ND; k++) put(ND + k, hiin(k));
+}
+
 // digit stream -> 32-bit words at RUN TIME (digits arrive inside a rolled loop):
 // each 52-bit digit joins the < 32 pending bits in a 64-bit buffer and whole
 // words leave through emit(v), in order (one or two per digit).

@@ -90,3 +90,22 @@ def test_runtime_word_emitter(model, op):
     rng = random.Random(13)
     for a, _ in operands(rng):
         assert model(f"{op} {a:x}") == a
+
+
+@pytest.mark.parametrize("op", ["B", "C"])
+def test_square_blocks(model, op):
+    """sqr_blocks: the rolled block triangle (blocks of 10 / 8 digits at ND = 40)."""
+    rng = random.Random(14)
+    for a, _ in operands(rng):
+        assert model(f"{op} {a:x}") == a * a
+
+
+def test_square_blocks_4096(model):
+    """sqr_blocks at the 4096-bit class's ND = 80 (the kernel's instance)."""
+    rng = random.Random(15)
+    top = (1 << 4096) - 1
+    cases = [top, 0, 1, 1 << 4095, (1 << 4160 - 1) & top, int("f" * 13, 16) << 52 * 70]
+    cases += [rng.getrandbits(4096) for _ in range(30)]
+    cases += [sum(rng.getrandbits(52) << (52 * k) for k in rng.sample(range(78), 6)) & top for _ in range(10)]
+    for a in cases:
+        assert model(f"G {a:x}") == a * a

@@ -10,6 +10,8 @@
 //   W x     x (64 words) -> 40 digits (words_to_digits) -> back to words (Packer)
 //   E x     x (64 words) -> 40 digits -> words again through the run-time WordEmitter
 //   P a b   A B as two row halves (mul_rows_f with NR = 20 on b_0..19 and b_20..39), summed
+//   B a     T = A^2 through sqr_blocks (rolled block triangle), ND = 40, blocks of 10 / 8 (B / C)
+//   G a     the 4096-bit class (ND = 80, a < 2^4096, 256 output words): sqr_blocks, blocks of 10
 #include <cfenv>
 #include <cstdint>
 #include <cstdio>
@@ -49,8 +51,8 @@ int main() {
         std::istringstream is(line);
         std::string op, x, y;
         is >> op >> x >> y;
-        uint32_t aw[NW], bw[NW], out[2 * NW];
-        parse_words(x, aw, NW);
+        uint32_t aw[2 * NW], bw[NW], out[4 * NW];
+        parse_words(x, aw, op == "G" ? 2 * NW : NW);
         parse_words(y.empty() ? "0" : y, bw, NW);
         double a[ND], b[ND];
         tcd::words_to_digits<ND>([&](int w) -> uint32_t { return w < NW ? aw[w] : 0u; }, a);
@@ -107,6 +109,34 @@ int main() {
                 if (op == "E") we.digit((uint64_t)a[k]);
                 else wes.digit((uint64_t)a[k]);
             }
+        } else if (op == "B" || op == "C") {
+            uint64_t low[ND], high[ND];
+            auto ag = [&](int i) { return a[i]; };
+            auto lo = [&](int c, uint64_t d) { low[c] = d; };
+            auto ho = [&](int k, uint64_t d) { high[k] = d; };
+            auto hi = [&](int k) { return high[k]; };
+            if (op == "B") tcd::sqr_blocks<ND, 10>(ag, lo, ho, hi, put);
+            else tcd::sqr_blocks<ND, 8>(ag, lo, ho, hi, put);
+            // put got columns ND.. only: the low columns through the packer first
+            tcd::Packer<2 * NW, decltype(word)> pk2{word, 0};
+            for (int k = 0; k < ND; k++) pk2.put(k, low[k]);
+            for (int k = ND; k < 2 * ND; k++) pk2.put(k, high[k - ND]);
+        } else if (op == "G") {
+            constexpr int N4 = 80;
+            double a4[N4];
+            uint64_t low[N4], high[N4];
+            tcd::words_to_digits<N4>([&](int w) -> uint32_t { return w < 2 * NW ? aw[w] : 0u; }, a4);
+            auto word4 = [&](int w, uint32_t v) { out[w] = v; };
+            tcd::Packer<4 * NW, decltype(word4)> pk4{word4, 0};
+            auto put4 = [&](int, uint64_t) {};
+            // high digit k overwrites A's digit k (block s - NB, dead), like the kernel's slot
+            tcd::sqr_blocks<N4, 10>([&](int i) { return a4[i]; }, [&](int c, uint64_t d) { low[c] = d; },
+                                    [&](int k, uint64_t d) { memcpy(&a4[k], &d, 8); },
+                                    [&](int k) { uint64_t d; memcpy(&d, &a4[k], 8); high[k] = d; return d; }, put4);
+            for (int k = 0; k < N4; k++) pk4.put(k, low[k]);
+            for (int k = N4; k < 2 * N4; k++) pk4.put(k, high[k - N4]);
+            print_words(out, 4 * NW);
+            continue;
         } else if (op == "W") {
             for (int k = 0; k < ND; k++) put(k, (uint64_t)a[k]);
             for (int k = ND; k < 2 * ND; k++) put(k, 0);
