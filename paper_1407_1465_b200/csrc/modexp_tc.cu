@@ -78,6 +78,12 @@ namespace rsa_b200 {
 #ifndef RSA_TC_SQBLK128
 #define RSA_TC_SQBLK128 10  // 4096-bit squarings by the rolled block triangle (tcd::sqr_blocks, blocks of this
 #endif                      // many digits; 3240 digit products instead of the row form's 6400; 0 = rows)
+// 4096-bit window multiplies by the rolled block product (tcd::mul_blocks, blocks of this many digits):
+// A/B 96.3K (10) / 95.5K (8) vs 98.9K decrypts/s for the row form, which loads one table digit per row
+// a row ahead; the blocks load B from global memory in bursts.  0 = rows (default).
+#ifndef RSA_TC_MULBLK128
+#define RSA_TC_MULBLK128 0
+#endif
 #ifndef RSA_TC_APAIR
 #define RSA_TC_APAIR 0      // 4096-bit A slot as digit pairs (A/B)
 #endif
@@ -352,7 +358,13 @@ __global__ void __launch_bounds__(TcCfg<S>::BLOCK, 1) modexp_tc_kernel(const __g
                                 const double2 v = table[((size_t)op.bidx * NP + (j >> 1)) * nthr + gtid];
                                 return (j & 1) ? v.y : v.x;
                             };
-                            tcd::mul_rows_f<ND, false>(get_digit_rows, btab, lout, lin, put);
+                            if constexpr (RSA_TC_MULBLK128 != 0) {
+                                auto hiout = [&](int k, uint64_t d) { *slot_at(k) = f64::from_bits(d); };
+                                auto hiin = [&](int k) -> uint64_t { return f64::bits(get_digit(k)); };
+                                tcd::mul_blocks<ND, RSA_TC_MULBLK128>(get_digit, btab, lout, hiout, hiin, put);
+                            } else {
+                                tcd::mul_rows_f<ND, false>(get_digit_rows, btab, lout, lin, put);
+                            }
                         } else {
                             tcd::mul_rows_f<ND, false>(get_digit_rows, bget, lout, lin, put);
                         }

@@ -194,6 +194,65 @@ __host__ __device__ __forceinline__ void sqr_blocks(AF a, LO lowout, HO hiout, H
     for (int k = 0; k < ND; k++) put(ND + k, hiin(k));
 }
 
+// mul_blocks: T = A B in the same rolled block structure (every block pair
+// (p, s - p) at step s, no doubling, no digit squares): column c finishes as
+// W_c - bias_c + carry with bias_c = nm(c) BL + nm(c - 1) BH, nm(c) =
+// #{i, j < ND : i + j = c}.  A's block s - NB is dead at step s (hiout may
+// overwrite it); b is only read.
+template <int ND, int BS, typename AF, typename BF, typename LO, typename HO, typename HI, typename Put>
+__host__ __device__ __forceinline__ void mul_blocks(AF a, BF b, LO lowout, HO hiout, HI hiin, Put put) {
+    static_assert(ND % BS == 0, "blocks");
+    constexpr int NB = ND / BS;
+    uint64_t w[2 * BS];
+#pragma unroll
+    for (int d = 0; d < 2 * BS; d++) w[d] = 0;
+    uint64_t carry = 0;
+    auto nm = [](int c) -> uint64_t {          // pairs i, j < ND with i + j = c
+        return (c < 0 || c > 2 * ND - 2) ? 0 : (uint64_t)((c < 2 * ND - 2 - c ? c : 2 * ND - 2 - c) + 1);
+    };
+#ifdef __CUDA_ARCH__
+#pragma unroll 1
+#endif
+    for (int s = 0; s < 2 * NB; s++) {
+        const int pmin = s - (NB - 1) > 0 ? s - (NB - 1) : 0, pend = s < NB - 1 ? s + 1 : NB;
+#ifdef __CUDA_ARCH__
+#pragma unroll 1
+#endif
+        for (int p = pmin; p < pend; p++) {
+            double x[BS], y[BS];
+#pragma unroll
+            for (int k = 0; k < BS; k++) {
+                x[k] = a(BS * p + k);
+                y[k] = b(BS * (s - p) + k);
+            }
+#pragma unroll
+            for (int i = 0; i < BS; i++) {
+                uint64_t hp = 0;
+#pragma unroll
+                for (int k = 0; k < BS; k++) {
+                    const double h = fma_rz(x[k], y[i], C104);
+                    const double l = fma_rz(x[k], y[i], sub_rn(C2, h));
+                    w[i + k] += bits(l) + hp;
+                    hp = bits(h);
+                }
+                w[i + BS] += hp;
+            }
+        }
+#pragma unroll
+        for (int d = 0; d < BS; d++) {
+            const int c = BS * s + d;
+            const uint64_t v = w[d] - (nm(c) * BL + nm(c - 1) * BH) + carry;
+            carry = v >> D;
+            if (c < ND) lowout(c, v & M52);
+            else hiout(c - ND, v & M52);
+            w[d] = w[d + BS];
+            w[d + BS] = 0;
+        }
+    }
+#pragma unroll
+    for (int k = 0; k < ND; k++) put(ND + k, hiin(k));
+}
+
 // digit stream -> 32-bit words at RUN TIME (digits arrive inside a rolled loop):
 // each 52-bit digit joins the < 32 pending bits in a 64-bit buffer and whole
 // words leave through emit(v), in order (one or two per digit).

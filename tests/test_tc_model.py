@@ -109,3 +109,22 @@ def test_square_blocks_4096(model):
     cases += [sum(rng.getrandbits(52) << (52 * k) for k in rng.sample(range(78), 6)) & top for _ in range(10)]
     for a in cases:
         assert model(f"G {a:x}") == a * a
+
+
+def test_product_blocks(model):
+    """mul_blocks: the rolled block product at ND = 40."""
+    rng = random.Random(16)
+    for a, b in operands(rng):
+        assert model(f"N {a:x} {b:x}") == a * b
+
+
+def test_product_blocks_4096(model):
+    """mul_blocks at ND = 80 with the kernel's slot aliasing (high digits over A)."""
+    rng = random.Random(17)
+    top = (1 << 4096) - 1
+    cases = [(top, top), (0, top), (1, 1), (top, 1), (1 << 4095, 1 << 4095)]
+    cases += [(rng.getrandbits(4096), rng.getrandbits(4096)) for _ in range(30)]
+    cases += [(sum(rng.getrandbits(52) << (52 * k) for k in rng.sample(range(78), 6)) & top,
+               sum(((1 << 32) - 1) << (32 * k) for k in rng.sample(range(128), 9))) for _ in range(10)]
+    for a, b in cases:
+        assert model(f"O {a:x} {b:x}") == a * b

@@ -11,6 +11,8 @@
 //   E x     x (64 words) -> 40 digits -> words again through the run-time WordEmitter
 //   P a b   A B as two row halves (mul_rows_f with NR = 20 on b_0..19 and b_20..39), summed
 //   B a     T = A^2 through sqr_blocks (rolled block triangle), ND = 40, blocks of 10 / 8 (B / C)
+//   N a b   T = A B through mul_blocks, ND = 40, blocks of 10
+//   O a b   mul_blocks at ND = 80 (4096-bit operands, high digits over A's dead blocks)
 //   G a     the 4096-bit class (ND = 80, a < 2^4096, 256 output words): sqr_blocks, blocks of 10
 #include <cfenv>
 #include <cstdint>
@@ -51,9 +53,10 @@ int main() {
         std::istringstream is(line);
         std::string op, x, y;
         is >> op >> x >> y;
-        uint32_t aw[2 * NW], bw[NW], out[4 * NW];
-        parse_words(x, aw, op == "G" ? 2 * NW : NW);
-        parse_words(y.empty() ? "0" : y, bw, NW);
+        uint32_t aw[2 * NW], bw[2 * NW], out[4 * NW];
+        const bool big = op == "G" || op == "O";
+        parse_words(x, aw, big ? 2 * NW : NW);
+        parse_words(y.empty() ? "0" : y, bw, big ? 2 * NW : NW);
         double a[ND], b[ND];
         tcd::words_to_digits<ND>([&](int w) -> uint32_t { return w < NW ? aw[w] : 0u; }, a);
         tcd::words_to_digits<ND>([&](int w) -> uint32_t { return w < NW ? bw[w] : 0u; }, b);
@@ -133,6 +136,30 @@ int main() {
             tcd::sqr_blocks<N4, 10>([&](int i) { return a4[i]; }, [&](int c, uint64_t d) { low[c] = d; },
                                     [&](int k, uint64_t d) { memcpy(&a4[k], &d, 8); },
                                     [&](int k) { uint64_t d; memcpy(&d, &a4[k], 8); high[k] = d; return d; }, put4);
+            for (int k = 0; k < N4; k++) pk4.put(k, low[k]);
+            for (int k = N4; k < 2 * N4; k++) pk4.put(k, high[k - N4]);
+            print_words(out, 4 * NW);
+            continue;
+        } else if (op == "N") {
+            uint64_t low[ND], high[ND];
+            tcd::mul_blocks<ND, 10>([&](int i) { return a[i]; }, [&](int j) { return b[j]; },
+                                    [&](int c, uint64_t d) { low[c] = d; }, [&](int k, uint64_t d) { high[k] = d; },
+                                    [&](int k) { return high[k]; }, [](int, uint64_t) {});
+            for (int k = 0; k < ND; k++) put(k, low[k]);
+            for (int k = ND; k < 2 * ND; k++) put(k, high[k - ND]);
+        } else if (op == "O") {
+            constexpr int N4 = 80;
+            double a4[N4], b4[N4];
+            uint64_t low[N4], high[N4];
+            tcd::words_to_digits<N4>([&](int w) -> uint32_t { return w < 2 * NW ? aw[w] : 0u; }, a4);
+            tcd::words_to_digits<N4>([&](int w) -> uint32_t { return w < 2 * NW ? bw[w] : 0u; }, b4);
+            auto word4 = [&](int w, uint32_t v) { out[w] = v; };
+            tcd::Packer<4 * NW, decltype(word4)> pk4{word4, 0};
+            tcd::mul_blocks<N4, 10>([&](int i) { return a4[i]; }, [&](int j) { return b4[j]; },
+                                    [&](int c, uint64_t d) { low[c] = d; },
+                                    [&](int k, uint64_t d) { memcpy(&a4[k], &d, 8); },
+                                    [&](int k) { uint64_t d; memcpy(&d, &a4[k], 8); high[k] = d; return d; },
+                                    [](int, uint64_t) {});
             for (int k = 0; k < N4; k++) pk4.put(k, low[k]);
             for (int k = N4; k < 2 * N4; k++) pk4.put(k, high[k - N4]);
             print_words(out, 4 * NW);
