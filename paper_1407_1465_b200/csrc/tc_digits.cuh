@@ -15,6 +15,8 @@
 #pragma once
 #include <stdint.h>
 
+#include <type_traits>
+
 #include "mont_f64.cuh"
 
 namespace rsa_b200 {
@@ -119,10 +121,6 @@ __host__ __device__ __forceinline__ void sqr_blocks(AF a, LO lowout, HO hiout, H
 #pragma unroll
     for (int d = 0; d < 2 * BS; d++) w[d] = 0;
     uint64_t carry = 0;
-    auto nl = [](int c) -> uint64_t {          // pairs i < j < ND with i + j = c
-        const int lo = c - ND + 1 > 0 ? c - ND + 1 : 0, hi = (c + 1) / 2;
-        return hi > lo ? (uint64_t)(hi - lo) : 0;
-    };
 #ifdef __CUDA_ARCH__
 #pragma unroll 1
 #endif
@@ -168,22 +166,35 @@ __host__ __device__ __forceinline__ void sqr_blocks(AF a, LO lowout, HO hiout, H
                 w[k1 + BS] += hp;
             }
         }
-        // finish columns BS s + d: the digit squares a_i^2, i = BS s / 2 + m
+        // finish columns c = BS s + d with the digit squares a_i^2, i = BS s / 2 + m.  Every
+        // column of a step lies on one side of ND (ND % BS == 0), where nl is linear:
+        //   c <  ND: nl(BS s + e) = (BS/2) s + (e+1)/2
+        //   c >= ND: nl(BS s + e) = ND - 1 - (BS/2) s + (e+1)/2 - e      (e = -1 .. BS-1)
+        // (the two agree at c = ND - 1), so bias_c = base_s (BL + BH) + a static constant.
+        auto finish = [&](auto hiside) {
+            constexpr bool HIGH = decltype(hiside)::value;
+            const uint64_t base = HIGH ? (uint64_t)(ND - 1 - (BS / 2) * s) : (uint64_t)((BS / 2) * s);
+            const uint64_t q2 = 2 * base * (BL + BH);
 #pragma unroll
-        for (int m = 0; m < BS / 2; m++) {
-            const double ai = a(BS * s / 2 + m);
-            const double h = fma_rz(ai, ai, C104);
-            const double l = fma_rz(ai, ai, sub_rn(C2, h));
+            for (int m = 0; m < BS / 2; m++) {
+                const double ai = a(BS * s / 2 + m);
+                const double h = fma_rz(ai, ai, C104);
+                const double l = fma_rz(ai, ai, sub_rn(C2, h));
 #pragma unroll
-            for (int e = 0; e < 2; e++) {
-                const int d = 2 * m + e, c = BS * s + d;
-                const uint64_t bias = nl(c) * BL + nl(c - 1) * BH;
-                const uint64_t v = 2 * (w[d] - bias) + (e ? bits(h) - BH : bits(l) - BL) + carry;
-                carry = v >> D;
-                if (c < ND) lowout(c, v & M52);
-                else hiout(c - ND, v & M52);
+                for (int e = 0; e < 2; e++) {
+                    const int d = 2 * m + e;
+                    constexpr auto g = [](int x) -> int64_t { return HIGH ? (x + 1) / 2 - x : (x + 1) / 2; };
+                    // 2 bias_c - 2 base (BL + BH) + the square half's exponent field
+                    const uint64_t k = 2 * ((uint64_t)g(d) * BL + (uint64_t)g(d - 1) * BH) + (e ? BH : BL);
+                    const uint64_t v = 2 * w[d] + (e ? bits(h) : bits(l)) + carry - q2 - k;
+                    carry = v >> D;
+                    if constexpr (HIGH) hiout(BS * s + d - ND, v & M52);
+                    else lowout(BS * s + d, v & M52);
+                }
             }
-        }
+        };
+        if (s < NB) finish(std::false_type{});
+        else finish(std::true_type{});
 #pragma unroll
         for (int d = 0; d < BS; d++) {
             w[d] = w[d + BS];
