@@ -79,7 +79,8 @@ namespace rsa_b200 {
 #define RSA_TC_SQBLK128 10  // 4096-bit squarings by the rolled block triangle (tcd::sqr_blocks, blocks of this
 #endif                      // many digits; 3240 digit products instead of the row form's 6400; 0 = rows)
 // 4096-bit window multiplies by the rolled block product (tcd::mul_blocks, blocks of this many digits):
-// A/B 96.3K (10) / 95.5K (8) vs 98.9K decrypts/s for the row form, which loads one table digit per row
+// A/B 96.3K (10) / 95.5K (8) vs 98.9K decrypts/s for the row form (102.5K vs 105.8K once both squaring
+// and multiply finish columns from per-step constants); the row form loads one table digit per row
 // a row ahead; the blocks load B from global memory in bursts.  0 = rows (default).
 #ifndef RSA_TC_MULBLK128
 #define RSA_TC_MULBLK128 0

@@ -208,7 +208,7 @@ __host__ __device__ __forceinline__ void sqr_blocks(AF a, LO lowout, HO hiout, H
 // mul_blocks: T = A B in the same rolled block structure (every block pair
 // (p, s - p) at step s, no doubling, no digit squares): column c finishes as
 // W_c - bias_c + carry with bias_c = nm(c) BL + nm(c - 1) BH, nm(c) =
-// #{i, j < ND : i + j = c}.  A's block s - NB is dead at step s (hiout may
+// #{i, j < ND : i + j = c} (a per-step base plus static constants).  A's block s - NB is dead at step s (hiout may
 // overwrite it); b is only read.
 template <int ND, int BS, typename AF, typename BF, typename LO, typename HO, typename HI, typename Put>
 __host__ __device__ __forceinline__ void mul_blocks(AF a, BF b, LO lowout, HO hiout, HI hiin, Put put) {
@@ -218,9 +218,6 @@ __host__ __device__ __forceinline__ void mul_blocks(AF a, BF b, LO lowout, HO hi
 #pragma unroll
     for (int d = 0; d < 2 * BS; d++) w[d] = 0;
     uint64_t carry = 0;
-    auto nm = [](int c) -> uint64_t {          // pairs i, j < ND with i + j = c
-        return (c < 0 || c > 2 * ND - 2) ? 0 : (uint64_t)((c < 2 * ND - 2 - c ? c : 2 * ND - 2 - c) + 1);
-    };
 #ifdef __CUDA_ARCH__
 #pragma unroll 1
 #endif
@@ -249,16 +246,26 @@ __host__ __device__ __forceinline__ void mul_blocks(AF a, BF b, LO lowout, HO hi
                 w[i + BS] += hp;
             }
         }
+        // nm is linear on each side of ND (as in sqr_blocks): c = BS s + e,
+        //   c < ND: nm = BS s + e + 1;   c >= ND: nm = 2 ND - 1 - BS s - e
+        auto finish = [&](auto hiside) {
+            constexpr bool HIGH = decltype(hiside)::value;
+            const uint64_t base = HIGH ? (uint64_t)(2 * ND - 1 - BS * s) : (uint64_t)(BS * s);
+            const uint64_t q = base * (BL + BH);
 #pragma unroll
-        for (int d = 0; d < BS; d++) {
-            const int c = BS * s + d;
-            const uint64_t v = w[d] - (nm(c) * BL + nm(c - 1) * BH) + carry;
-            carry = v >> D;
-            if (c < ND) lowout(c, v & M52);
-            else hiout(c - ND, v & M52);
-            w[d] = w[d + BS];
-            w[d + BS] = 0;
-        }
+            for (int d = 0; d < BS; d++) {
+                constexpr auto g = [](int x) -> int64_t { return HIGH ? -x : x + 1; };
+                const uint64_t k = (uint64_t)g(d) * BL + (uint64_t)g(d - 1) * BH;
+                const uint64_t v = w[d] + carry - q - k;
+                carry = v >> D;
+                if constexpr (HIGH) hiout(BS * s + d - ND, v & M52);
+                else lowout(BS * s + d, v & M52);
+                w[d] = w[d + BS];
+                w[d + BS] = 0;
+            }
+        };
+        if (s < NB) finish(std::false_type{});
+        else finish(std::true_type{});
     }
 #pragma unroll
     for (int k = 0; k < ND; k++) put(ND + k, hiin(k));
